@@ -1,0 +1,367 @@
+#!/usr/bin/env python
+"""Throughput benchmark of the B200 directional-filter path (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A "step" is one filter pass over one frame (or the frame batch for c5b) of a
+BASELINE config's seeded synthetic input, resident in HBM.  The default
+workload is BASELINE.json configs[1] (C2: DDF 3x3 exact on a 1024x1024
+image, 15% uncorrelated impulsive noise); ``--config`` selects the others
+(c1, c3, c4_*, c5a, c5b; see paper_1009_0958_b200/synth.py).
+
+Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
+events on the launching stream; an L2 flush (a 256 MiB device write) runs
+between timed steps, outside the events, so no step reads its input from a
+warm L2.  The K-step region is bracketed by a barrier and
+torch.cuda.synchronize() on both sides; the step time is the MAX over ranks.
+nvidia-smi samples SM clocks and throttle reasons during the timed region.
+
+Multi-GPU (torchrun, one process per GPU): c1-c4 run one replica per rank
+(weak scaling: every rank filters its own frame); c5a shards the 8192-row
+frame into contiguous row strips, each rank holding its strip plus a 3-row
+halo (strong scaling, no collective on the data path); c5b splits the 64
+frames across ranks (strong).
+
+``--impl reference`` times the reference algorithm's CPU implementation on
+the host cores instead: the float64 C restatement in oracle/ (the reference
+itself is Python+numba and cannot travel to the GPU box), all host threads,
+on bounded row bands of the same input.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1009_0958_b200 import synth  # noqa: E402
+from paper_1009_0958_b200.spec import parse_filter_spec  # noqa: E402
+
+# canonical algorithmic work per output pixel (FMA-pipe lane
+# ops, MUFU ops) -- U = ((2s-1)^2 - 1)/2 unique pair offsets x per-pair cost
+# + n(n-1) aggregation adds per aggregate (+ DDF/ACWDDF selection terms).
+WORK = {
+    "c1": (264, 12), "c2": (417, 24), "c3": (2333, 80),
+    "c4_bvdf_minimax": (920, 40), "c4_bvdf_rgb": (840, 40), "c4_ddf_minimax": (1785, 80),
+    "c4_ddf_rgb": (1705, 80), "c5a": (6601, 168), "c5b": (501, 24),
+}
+BYTES_PER_PX = 6  # 3 B uint8 in + 3 B uint8 out (halo re-reads excluded)
+
+
+def peaks():
+    """FP32 FMA-pipe peak (148 SMs x 128 lanes x max SM clock) and measured HBM."""
+    sm_mhz, hbm = 1965.0, 6552.0
+    src = "MEASURED_PEAKS.json"
+    try:
+        mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        sm_mhz = float(mp.get("sm_max_mhz", sm_mhz))
+        hbm = float(mp.get("hbm_gbs", hbm))
+    except Exception:
+        src = "fallback (B200_PROFILING.md)"
+        hbm = 6650.0
+    return 148 * 128 * sm_mhz * 1e6, hbm, sm_mhz, src
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.05)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def workload(config: str, rank: int, world: int):
+    """(input array for this rank, output pixels of this rank, total pixels, description)."""
+    cfg = synth.CONFIGS[config]
+    H, W = cfg["shape"]
+    if config == "c5b":
+        B = cfg["frames"]
+        per = math.ceil(B / world)
+        f0, f1 = rank * per, min(B, (rank + 1) * per)
+        frames = np.stack([synth.noisy_image(H, W, cfg["seed"] + i, cfg["noise"]) for i in range(f0, f1)])
+        return {"kind": "batch", "x": frames, "px": frames.shape[0] * H * W, "total_px": B * H * W,
+                "scaling": "strong" if world > 1 else "weak"}
+    img = synth.config_input(config)
+    if config == "c5a" and world > 1:
+        h = parse_filter_spec(cfg["spec"]).window // 2
+        per = math.ceil(H / world)
+        r0, r1 = rank * per, min(H, (rank + 1) * per)
+        i0, i1 = max(0, r0 - h), min(H, r1 + h)
+        return {"kind": "rows", "x": np.ascontiguousarray(img[i0:i1]), "in_row0": i0, "out_row0": r0,
+                "out_rows": r1 - r0, "H": H, "px": (r1 - r0) * W, "total_px": H * W, "scaling": "strong"}
+    return {"kind": "image", "x": img, "px": H * W, "total_px": H * W * world, "scaling": "weak"}
+
+
+def cpu_rate(img: np.ndarray, spec, budget_s: float, threads: int, min_rows: int = 4):
+    """Time the float64 oracle (the reference algorithm restated in C) on
+    full-width row bands of ``img`` for about ``budget_s`` seconds."""
+    import oracle
+
+    H, W = img.shape[:2]
+    rows = min(H, min_rows)
+    t0 = time.perf_counter()
+    oracle.filter_image(img, spec, threads=threads, rows=(0, rows))
+    dt = time.perf_counter() - t0
+    rows2 = int(min(H, max(rows, rows * budget_s / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.filter_image(img, spec, threads=threads, rows=(0, rows2))
+    dt = time.perf_counter() - t0
+    return rows2 * W / dt / 1e6, rows2, dt
+
+
+def run_reference(args, config):
+    """--impl reference: the reference algorithm on the host cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[config]
+    spec = parse_filter_spec(cfg["spec"])
+    img = synth.config_input(config, frames=1)
+    if img.ndim == 4:
+        img = img[0]
+    H, W = img.shape[:2]
+    threads = os.cpu_count() or 1
+    # size each step so the whole --steps/--warmup run stays within ~2 minutes
+    per_step_s = max(0.5, min(10.0, 120.0 / (args.steps + args.warmup)))
+    _, rows, _ = cpu_rate(img, spec, per_step_s, threads)
+    times = []
+    for k in range(args.warmup + args.steps):
+        r0 = (k * rows) % max(1, H - rows + 1)
+        t0 = time.perf_counter()
+        import oracle
+
+        oracle.filter_image(img, spec, threads=threads, rows=(r0, r0 + rows))
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            times.append(dt)
+    px = rows * W
+    value = px * len(times) / sum(times) / 1e6
+    line = {
+        "impl": "reference", "metric": "Mpixel/s per filter/window", "value": round(value, 4),
+        "unit": "Mpixel/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d))",
+        "config": {"workload": config, "spec": cfg["spec"], "shape": list(cfg["shape"]),
+                   "sample_rows_per_step": rows},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel/s", "cores": threads, "kind": "port",
+                         "sample": f"{rows} full-width rows x {W} px of the {config} frame per step "
+                                   f"(oracle/oracle.c: the reference engine restated in C, glibc acos)"},
+        "e2e": {"value": round(value, 4), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, config):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1009_0958_b200 import filters as F
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = synth.CONFIGS[config]
+    spec = parse_filter_spec(cfg["spec"])
+    wl = workload(config, rank, world)
+    x = torch.from_numpy(wl["x"]).to(dev)
+    out = torch.empty_like(x) if wl["kind"] != "rows" else torch.empty((wl["out_rows"],) + tuple(x.shape[1:]),
+                                                                       dtype=torch.uint8, device=dev)
+    from paper_1009_0958_b200 import _lib
+
+    ws_buf = torch.empty(_lib.lib().dfg_workspace_bytes(wl["px"]), dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        if wl["kind"] == "image":
+            F.filter_device(x, spec, out=out, ws=ws_buf)
+        elif wl["kind"] == "batch":
+            F.filter_batch_device(x, spec, out=out, ws=ws_buf)
+        else:
+            F.filter_rows_device(x, wl["H"], wl["in_row0"], wl["out_row0"], wl["out_rows"], spec, out=out, ws=ws_buf)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    import ctypes
+
+    cnt = ctypes.c_int64(0)
+    _lib.check(_lib.lib().dfg_fixup_count(ctypes.c_void_p(ws_buf.data_ptr()), None, ctypes.byref(cnt)))
+    redecided = int(cnt.value)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush.fill_(k & 0xff)
+            starts[k].record()
+            step()
+            ends[k].record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    tot = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    tot_ms = float(tot.item())
+    ms_step = tot_ms / args.steps
+    value = wl["total_px"] / (ms_step / 1e3) / 1e6  # Mpixel/s, whole job
+
+    # end to end through the C ABI's host path (pinned host buffers, H2D + D2H inside)
+    e2e = None
+    if wl["kind"] == "image":
+        hin = torch.from_numpy(wl["x"]).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        a_in, a_out = hin.numpy(), hout.numpy()
+        for _ in range(max(1, args.warmup)):
+            F.filter_host(a_in, spec, out=a_out)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            F.filter_host(a_in, spec, out=a_out)
+        e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+        et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e_ms = float(et.item())
+        nb = int(np.prod(wl["x"].shape))
+        e2e = {"value": round(wl["total_px"] / (e_ms / 1e3) / 1e6, 3), "unit": "Mpixel/s",
+               "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb, "ms_per_step": round(e_ms, 4),
+               "path": "dfg_filter_host (C ABI, pinned host buffers, synchronous)"}
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak_fma, hbm_peak, sm_mhz, peak_src = peaks()
+    fma_px, mufu_px = WORK[config]
+    px_per_s_gpu = wl["px"] / (ms_step / 1e3)
+    achieved = px_per_s_gpu * fma_px / 1e12
+    roofline = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak_fma / 1e12, 3),
+                "unit": "T FMA-pipe lane-ops/s", "frac": round(achieved * 1e12 / peak_fma, 4), "traffic": None,
+                "per_px": {"fma": fma_px, "mufu": mufu_px},
+                "note": "SURVEY 8(d) canonical work per pixel / whole-step device time (decision kernel + float64 "
+                        f"re-decision + workspace reset); peak = 148 SM x 128 lanes x {sm_mhz:.0f} MHz ({peak_src})",
+                "hbm": {"achieved": round(px_per_s_gpu * BYTES_PER_PX / 1e9, 2), "peak": hbm_peak, "unit": "GB/s",
+                        "frac": round(px_per_s_gpu * BYTES_PER_PX / 1e9 / hbm_peak, 5)}}
+    # CPU baseline: the oracle on a bounded sample of the same workload
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        img = wl["x"][0] if wl["x"].ndim == 4 else wl["x"]
+        threads = os.cpu_count() or 1
+        rate, rows, dt = cpu_rate(img, spec, args.cpu_seconds, threads)
+        cpu = {"value": round(rate, 4), "unit": "Mpixel/s", "cores": threads, "kind": "port",
+               "sample": f"{rows} full-width rows ({rows * img.shape[1]} px) of the {config} frame, {dt:.1f} s, "
+                         "oracle/oracle.c (reference engine restated in C, float64, glibc acos)"}
+    launches = args.steps * 2  # decision kernel + float64 re-decision kernel per step
+    line = {
+        "metric": "Mpixel/s per filter/window", "value": round(value, 3), "unit": "Mpixel/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f32+f64 (u8 io)",
+        "data": "synthetic (seeded gradient + 20 rectangles + impulsive noise, SURVEY 8(d))",
+        "config": {"workload": config, "spec": cfg["spec"], "shape": list(cfg["shape"]),
+                   "noise": list(cfg["noise"]), "seed": cfg["seed"], "frames": cfg.get("frames", 1),
+                   "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"{wl['kind']} x{world}"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "redecided_px_per_step": redecided, "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args, args.config)
+    else:
+        run_ours(args, args.config)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,146 @@
+/*
+ * dirfilt_gpu.h -- C ABI of the B200 (sm_100a) directional vector filter path.
+ *
+ * Drop-in boundary for the reference's whole-image driver:
+ *
+ *   reference                                     replaced by
+ *   --------------------------------------------  -------------------------------
+ *   filters.apply_filter            filters.py:379-433   dfg_filter / dfg_filter_host
+ *   _engine.EnginePlanes (prep)     _engine.py:513-557   staging stage inside dfg_filter
+ *   _engine.run_rows(.., r0, r1)    _engine.py:560-583   dfg_filter_rows (row band)
+ *   apply_filter(workers=k) bands   filters.py:416-430   dfg_filter_rows per GPU strip
+ *   (frame loop in bench/CLI)       bench.py:96-109      dfg_filter_batch
+ *
+ * The reference has no FFI of its own (pure Python + numba); these entry
+ * points are what its filters.py would bind through ctypes -- INTEGRATION.md
+ * shows that binding.  Plain C types only: device pointers, sizes, one POD
+ * parameter struct, an opaque cudaStream_t passed as void*.
+ *
+ * Images are uint8 RGB, interleaved (H, W, 3), row pitch in bytes.  The
+ * reference's float64 RasterImage holding integers 0..255 maps onto this
+ * losslessly; non-integral or >255 pixels are rejected by the host shim.
+ *
+ * Results are the reference's selections: every output pixel is the input
+ * pixel the reference's float64 engine selects for that window.  The fast
+ * FP32 kernel decides every pixel whose decision margin exceeds its
+ * rigorous error budget; the rest are re-decided by a float64 kernel that
+ * repeats the reference's operation order ("Exactness").
+ *
+ * Every call returns 0 on success or a negative DFG_E* code; the message is
+ * available from dfg_last_error() (thread-local).  Calls are stateless,
+ * re-entrant per stream, and do not allocate (except dfg_filter_host, which
+ * keeps a per-thread cached device staging buffer).
+ */
+#ifndef DIRFILT_GPU_H
+#define DIRFILT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFG_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define DFG_API __attribute__((visibility("default")))
+#else
+#define DFG_API
+#endif
+
+/* family: filters.py:34 FAMILIES */
+#define DFG_IDENTITY 0
+#define DFG_VMF 1
+#define DFG_BVDF 2
+#define DFG_DDF 3
+#define DFG_ACWDDF 4
+
+/* strategy: filters.py:37-82 DirectionalStrategy.kind, _engine.py:25-28 */
+#define DFG_EXACT 0
+#define DFG_MINIMAX 1
+#define DFG_CHROMA 2
+
+/* border: image.py:32-55 BorderPolicy (replicate = np.pad edge, reflect = symmetric) */
+#define DFG_REPLICATE 0
+#define DFG_REFLECT 1
+
+/* error codes */
+#define DFG_OK 0
+#define DFG_E_ARG (-1)     /* invalid argument (maps to the reference's ValueError) */
+#define DFG_E_CUDA (-2)    /* CUDA runtime error */
+#define DFG_E_UNSUP (-3)   /* valid spec outside this build (e.g. window > 7) */
+#define DFG_E_WS (-4)      /* workspace too small */
+
+/* Mirrors FilterSpec (filters.py:126-151) + AcwddfParams (filters.py:97-123)
+ * + the engine's padded coefficient tuples (_engine.py:504-510). */
+typedef struct dfg_params {
+    int32_t family;
+    int32_t strategy;
+    int32_t window;      /* odd side s; this build: 3, 5, 7 */
+    int32_t border;
+    double p;            /* Minkowski order: spec.p, or acwddf.p for ACWDDF (filters.py:398) */
+    double asin_c[5];    /* ASIN polynomial a0..a4, zero-padded (minimax only) */
+    double acos_c[5];    /* ACOS polynomial a0..a4, zero-padded (minimax only) */
+    int32_t lam;         /* ACWDDF smoothing level lambda (>= 1, lambda + 2 <= (n+1)/2) */
+    int32_t reserved;
+    double threshold;    /* ACWDDF switching threshold T */
+    double slope;        /* chromaticity calibration (ACWDDF switching sum only) */
+    double intercept;
+} dfg_params;
+
+DFG_API int dfg_abi_version(void);
+DFG_API const char *dfg_last_error(void);
+
+/* Device workspace needed to filter up to n_pixels output pixels per call. */
+DFG_API size_t dfg_workspace_bytes(int64_t n_pixels);
+
+/* Whole image: d_in (H, W, 3) -> d_out (H, W, 3), both device memory. */
+DFG_API int dfg_filter(const uint8_t *d_in, int32_t H, int32_t W, int64_t in_pitch,
+               uint8_t *d_out, int64_t out_pitch, const dfg_params *prm,
+               void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* Row band of an image of global_H rows (multi-GPU strips, reference
+ * run_rows(r0, r1)).  d_in holds global rows [in_row0, in_row0 + in_rows);
+ * it must include every row the border policy resolves for output rows
+ * [out_row0, out_row0 + out_rows) (for replicate: a halo of s/2 rows
+ * clipped to the image).  d_out receives exactly out_rows rows. */
+DFG_API int dfg_filter_rows(const uint8_t *d_in, int32_t global_H, int32_t W,
+                    int32_t in_row0, int32_t in_rows, int64_t in_pitch,
+                    uint8_t *d_out, int32_t out_row0, int32_t out_rows, int64_t out_pitch,
+                    const dfg_params *prm, void *d_workspace, size_t workspace_bytes,
+                    void *stream);
+
+/* B independent frames of (H, W, 3), frame strides in bytes. */
+DFG_API int dfg_filter_batch(const uint8_t *d_in, int32_t B, int32_t H, int32_t W,
+                     int64_t in_pitch, int64_t in_frame_stride,
+                     uint8_t *d_out, int64_t out_pitch, int64_t out_frame_stride,
+                     const dfg_params *prm, void *d_workspace, size_t workspace_bytes,
+                     void *stream);
+
+/* End to end from HOST memory (pinned or pageable): H2D, filter, D2H on
+ * `stream`, synchronised before return.  Device buffers are cached per
+ * calling thread and grown on demand. */
+DFG_API int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out,
+                    const dfg_params *prm, void *stream);
+
+/* Number of pixels the last call on this workspace re-decided in float64
+ * (synchronous read of the workspace counter). */
+DFG_API int dfg_fixup_count(const void *d_workspace, void *stream, int64_t *count);
+
+/* Diagnostics: the FP32 selection value of every window candidate
+ * (n floats per pixel, window order) as the fast kernel computes them, for
+ * error-budget validation against the float64 oracle.  d_vals: H*W*n floats. */
+DFG_API int dfg_debug_values(const uint8_t *d_in, int32_t H, int32_t W, int64_t in_pitch,
+                     float *d_vals, const dfg_params *prm, void *stream);
+
+/* Host-side double-double acos used by the float64 re-decision kernel, for
+ * CPU verification against libm: starts from libm acos(z) moved by
+ * perturb_ulps and refines. */
+DFG_API double dfg_cr_acos_host(double z, int32_t perturb_ulps);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DIRFILT_GPU_H */

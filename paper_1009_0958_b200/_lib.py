@@ -1,0 +1,126 @@
+"""ctypes binding of the in-tree CUDA library ``libdfg.so`` (C ABI in
+``include/dirfilt_gpu.h``).  There is no fallback: if the library is missing
+or cannot be loaded, every filter call raises."""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+from .spec import ACOS_COEFFICIENTS, ASIN_COEFFICIENTS
+
+LIB_PATH = Path(__file__).resolve().parent / "libdfg.so"
+
+DFG_OK, DFG_E_ARG, DFG_E_CUDA, DFG_E_UNSUP, DFG_E_WS = 0, -1, -2, -3, -4
+FAMILY_CODE = {"identity": 0, "vmf": 1, "bvdf": 2, "ddf": 3, "acwddf": 4}
+STRATEGY_CODE = {"exact": 0, "minimax": 1, "chromaticity": 2}
+BORDER_CODE = {"replicate": 0, "reflect": 1}
+
+# every symbol include/dirfilt_gpu.h declares
+EXPORTS = (
+    "dfg_abi_version", "dfg_last_error", "dfg_workspace_bytes", "dfg_filter",
+    "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_fixup_count",
+    "dfg_debug_values", "dfg_cr_acos_host",
+)
+
+
+class DfgParams(ctypes.Structure):
+    _fields_ = [
+        ("family", ctypes.c_int32),
+        ("strategy", ctypes.c_int32),
+        ("window", ctypes.c_int32),
+        ("border", ctypes.c_int32),
+        ("p", ctypes.c_double),
+        ("asin_c", ctypes.c_double * 5),
+        ("acos_c", ctypes.c_double * 5),
+        ("lam", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("threshold", ctypes.c_double),
+        ("slope", ctypes.c_double),
+        ("intercept", ctypes.c_double),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdfg.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_1009_0958_b200.build` "
+                           "(the GPU path has no CPU fallback)")
+    L = ctypes.CDLL(str(LIB_PATH))
+    vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    P = ctypes.POINTER(DfgParams)
+    L.dfg_abi_version.restype = ctypes.c_int
+    L.dfg_last_error.restype = ctypes.c_char_p
+    L.dfg_workspace_bytes.argtypes = [i64]
+    L.dfg_workspace_bytes.restype = sz
+    L.dfg_filter.argtypes = [vp, i32, i32, i64, vp, i64, P, vp, sz, vp]
+    L.dfg_filter_rows.argtypes = [vp, i32, i32, i32, i32, i64, vp, i32, i32, i64, P, vp, sz, vp]
+    L.dfg_filter_batch.argtypes = [vp, i32, i32, i32, i64, i64, vp, i64, i64, P, vp, sz, vp]
+    L.dfg_filter_host.argtypes = [vp, i32, i32, vp, P, vp]
+    L.dfg_fixup_count.argtypes = [vp, vp, ctypes.POINTER(i64)]
+    L.dfg_debug_values.argtypes = [vp, i32, i32, i64, vp, P, vp]
+    L.dfg_cr_acos_host.argtypes = [ctypes.c_double, i32]
+    L.dfg_cr_acos_host.restype = ctypes.c_double
+    for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host",
+                 "dfg_fixup_count", "dfg_debug_values"):
+        getattr(L, name).restype = ctypes.c_int
+    if L.dfg_abi_version() != 1:
+        raise RuntimeError("libdfg.so ABI version mismatch; rebuild")
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc == DFG_OK:
+        return
+    msg = lib().dfg_last_error().decode(errors="replace")
+    if rc == DFG_E_ARG:
+        raise ValueError(msg)
+    if rc == DFG_E_UNSUP:
+        raise NotImplementedError(msg)
+    raise RuntimeError(f"libdfg error {rc}: {msg}")
+
+
+def _pad5(t):
+    t = tuple(float(x) for x in t)
+    return t + (0.0,) * (5 - len(t))
+
+
+def params_from_spec(spec, policy) -> DfgParams:
+    """Pack a FilterSpec (this package's or the reference's) + BorderPolicy."""
+    prm = DfgParams()
+    fam = spec.family
+    if fam not in FAMILY_CODE:
+        raise ValueError(f"unknown engine family {fam!r}")
+    prm.family = FAMILY_CODE[fam]
+    kind = spec.strategy.kind
+    prm.strategy = STRATEGY_CODE[kind] if fam != "vmf" else 0
+    prm.window = int(spec.window)
+    mode = getattr(policy, "mode", policy)
+    prm.border = BORDER_CODE[mode]
+    if fam == "acwddf":
+        prm.p = float(spec.acwddf.p)
+        prm.lam = int(spec.acwddf.lam)
+        prm.threshold = float(spec.acwddf.threshold)
+    else:
+        prm.p = float(spec.p)
+        prm.lam = 2
+        prm.threshold = 10.8
+    if kind == "minimax" and fam != "vmf":
+        table = spec.strategy.table  # reference and this package both expose it
+        if table is not None:
+            cs, ca = table.asin_poly.coefficients, table.acos_poly.coefficients
+        else:
+            q = int(spec.strategy.q)
+            cs, ca = ASIN_COEFFICIENTS[q][1], ACOS_COEFFICIENTS[q][1]
+        prm.asin_c[:] = _pad5(cs)
+        prm.acos_c[:] = _pad5(ca)
+    prm.slope = float(spec.strategy.slope)
+    prm.intercept = float(spec.strategy.intercept)
+    return prm

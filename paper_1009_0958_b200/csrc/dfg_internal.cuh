@@ -1,0 +1,87 @@
+// dfg_internal.cuh -- shared device-side definitions for the directional
+// filter kernels (fast FP32 decision kernel + float64 re-decision kernel).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dirfilt_gpu.h"
+
+namespace dfg {
+
+enum { FAM_VMF = 1, FAM_BVDF = 2, FAM_DDF = 3, FAM_ACWDDF = 4 };
+enum { ST_EXACT = 0, ST_MINIMAX = 1, ST_CHROMA = 2 };
+enum { PC_2 = 0, PC_1 = 1, PC_GEN = 2 };  // Minkowski order: p == 2, p == 1, general
+
+// Kernel-side parameter block, passed by value.
+struct KParams {
+    // geometry (rows are global image rows; see dfg_filter_rows)
+    int global_H, W;
+    int in_row0, in_rows;
+    int out_row0, out_rows;
+    long long in_pitch, out_pitch, in_fstride, out_fstride;
+    int border;
+    int n_frames;
+    // FP32 copies of the spec constants
+    float p, invp;
+    float cs[5], ca[5];
+    float self_term;
+    float slope, intercept, threshold;
+    float w[3];  // ACWDDF extra centre weights n - 2k + 1, k = lam..lam+2
+    // rigorous error budget of one FP32 aggregate against the reference's
+    // float64 value: |agg32 - agg64| <= er * |agg| + ea   (angular term);
+    // Minkowski aggregates carry er only.  ea_pair: one angular pair.
+    float er, ea, ea_pair;
+    // float64 constants (seam recompute in the minimax route)
+    double cs64[5], ca64[5];
+    // pixels needing the float64 re-decision
+    unsigned *flag_count;
+    unsigned *flag_list;
+    // diagnostics: 2n floats per pixel (angular aggregates, Minkowski aggregates)
+    float *dbg;
+};
+
+// Extra parameters of the float64 re-decision kernel.
+struct FParams {
+    int family, strategy, window;
+    double p, self_term;
+    double cs[5], ca[5];
+    int lam;
+    double threshold, slope, intercept;
+};
+
+// Border policy resolution (image.py:158-176): replicate = clamp,
+// reflect = numpy 'symmetric' (edge-inclusive mirror, periodic).
+__host__ __device__ __forceinline__ int resolve_idx(int i, int size, int border)
+{
+    if (border == DFG_REPLICATE) return i < 0 ? 0 : (i >= size ? size - 1 : i);
+    if (size == 1) return 0;
+    int period = 2 * size;
+    i %= period;
+    if (i < 0) i += period;
+    return i < size ? i : period - 1 - i;
+}
+
+}  // namespace dfg
+
+// Launchers defined per instantiation unit (fast_s*.cu); return a cudaError_t.
+#define DFG_DECLARE_LAUNCH(S, FAMNAME)                                                         \
+    cudaError_t dfg_launch_s##S##_##FAMNAME(int strategy, int pcode, cudaStream_t st,           \
+                                            const uint8_t *in, uint8_t *out,                   \
+                                            const dfg::KParams &kp);
+
+DFG_DECLARE_LAUNCH(3, vmf)
+DFG_DECLARE_LAUNCH(3, bvdf)
+DFG_DECLARE_LAUNCH(3, ddf)
+DFG_DECLARE_LAUNCH(3, acwddf)
+DFG_DECLARE_LAUNCH(5, vmf)
+DFG_DECLARE_LAUNCH(5, bvdf)
+DFG_DECLARE_LAUNCH(5, ddf)
+DFG_DECLARE_LAUNCH(5, acwddf)
+DFG_DECLARE_LAUNCH(7, vmf)
+DFG_DECLARE_LAUNCH(7, bvdf)
+DFG_DECLARE_LAUNCH(7, ddf)
+DFG_DECLARE_LAUNCH(7, acwddf)
+
+cudaError_t dfg_launch_fixup(const uint8_t *in, uint8_t *out, const dfg::KParams &kp,
+                             const dfg::FParams &fp, cudaStream_t st);

@@ -1,0 +1,3 @@
+// Instantiation unit: window 3x3, BVDF (_engine.py:421-432).
+#include "dfg_fast.cuh"
+DFG_DEFINE_LAUNCH_BVDF(3)

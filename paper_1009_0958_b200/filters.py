@@ -1,0 +1,208 @@
+"""Whole-image directional filtering on the B200 -- the drop-in for the
+reference's ``apply_filter`` (reference ``pkg/src/dirfilt/filters.py:379-433``).
+
+``apply_filter(img, spec, policy=REPLICATE, workers=1)`` keeps the
+reference's signature, argument meaning and errors and returns a new
+``RasterImage`` whose every pixel is the input pixel the reference selects.
+Work happens in ``libdfg.so`` (hand-written sm_100a kernels) through the C
+ABI; PyTorch only provides device buffers and the current stream.  There is
+no CPU fallback: without a CUDA device or without the built library every
+call raises ``RuntimeError``.
+
+Device-resident entry points for pipelines (inputs already in HBM):
+``filter_device`` (one (H, W, 3) uint8 tensor), ``filter_batch_device``
+((B, H, W, 3)), ``filter_rows_device`` (a row strip of a taller image, used by
+the multi-GPU strip sharding in ``parallel.py``), and ``filter_host`` (the C
+ABI's host-buffer path: H2D + filter + D2H in one call).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+
+import numpy as np
+
+from . import _lib
+from .image import REPLICATE, RasterImage, to_uint8
+
+_ws_lock = threading.Lock()
+_ws_cache: dict = {}
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1009_0958_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
+    return torch
+
+
+def _validate_spec(spec) -> None:
+    """Re-run the reference's construction-time checks on duck-typed specs."""
+    fam = spec.family
+    if fam not in _lib.FAMILY_CODE:
+        raise ValueError(f"unknown filter family {fam!r}")
+    if fam == "identity":
+        return
+    if not float(spec.p) >= 1.0:
+        raise ValueError(f"Minkowski order must be >= 1, got {spec.p}")
+    w = int(spec.window)
+    if w < 3 or w % 2 == 0:
+        raise ValueError(f"window side must be odd and >= 3, got {w}")
+    if fam == "acwddf":
+        if spec.acwddf is None:
+            raise ValueError("acwddf parameters are required exactly when family is acwddf")
+        n = w * w
+        if spec.acwddf.lam + 2 > (n + 1) // 2:
+            raise ValueError(f"lambda {spec.acwddf.lam} too large for a window of {n} vectors")
+
+
+def workspace(nbytes: int, device=None):
+    """A cached device workspace of at least ``nbytes`` for ``device``."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
+    with _ws_lock:
+        buf = _ws_cache.get(dev.index)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            _ws_cache[dev.index] = buf
+        return buf
+
+
+def _stream_ptr(torch, stream, device):
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def filter_device(x, spec, policy=REPLICATE, out=None, stream=None, ws=None):
+    """Filter a CUDA uint8 tensor (H, W, 3) (row stride may be padded)."""
+    torch = _torch()
+    _validate_spec(spec)
+    if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[2] != 3 or not x.is_cuda:
+        raise ValueError("expected a CUDA uint8 tensor of shape (H, W, 3)")
+    if x.stride(2) != 1 or x.stride(1) != 3:
+        x = x.contiguous()
+    H, W = int(x.shape[0]), int(x.shape[1])
+    if out is None:
+        out = torch.empty((H, W, 3), dtype=torch.uint8, device=x.device)
+    prm = _lib.params_from_spec(spec, policy)
+    need = _lib.lib().dfg_workspace_bytes(H * W)
+    if ws is None:
+        ws = workspace(need, x.device)
+    with torch.cuda.device(x.device):
+        rc = _lib.lib().dfg_filter(ctypes.c_void_p(x.data_ptr()), H, W, x.stride(0),
+                                   ctypes.c_void_p(out.data_ptr()), out.stride(0), ctypes.byref(prm),
+                                   ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                   _stream_ptr(torch, stream, x.device))
+    _lib.check(rc)
+    return out
+
+
+def filter_batch_device(x, spec, policy=REPLICATE, out=None, stream=None, ws=None):
+    """Filter B frames at once: CUDA uint8 tensor (B, H, W, 3)."""
+    torch = _torch()
+    _validate_spec(spec)
+    if x.dtype != torch.uint8 or x.dim() != 4 or x.shape[3] != 3 or not x.is_cuda:
+        raise ValueError("expected a CUDA uint8 tensor of shape (B, H, W, 3)")
+    x = x.contiguous()
+    B, H, W = (int(s) for s in x.shape[:3])
+    if out is None:
+        out = torch.empty_like(x)
+    prm = _lib.params_from_spec(spec, policy)
+    need = _lib.lib().dfg_workspace_bytes(B * H * W)
+    if ws is None:
+        ws = workspace(need, x.device)
+    with torch.cuda.device(x.device):
+        rc = _lib.lib().dfg_filter_batch(ctypes.c_void_p(x.data_ptr()), B, H, W, x.stride(1), x.stride(0),
+                                         ctypes.c_void_p(out.data_ptr()), out.stride(1), out.stride(0),
+                                         ctypes.byref(prm), ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                         _stream_ptr(torch, stream, x.device))
+    _lib.check(rc)
+    return out
+
+
+def filter_rows_device(x, global_H, in_row0, out_row0, out_rows, spec, policy=REPLICATE,
+                       out=None, stream=None, ws=None):
+    """Filter output rows [out_row0, out_row0 + out_rows) of an image with
+    ``global_H`` rows, from a CUDA strip ``x`` holding global rows
+    [in_row0, in_row0 + x.shape[0]) (reference ``run_rows(r0, r1)``,
+    ``_engine.py:560-583``)."""
+    torch = _torch()
+    _validate_spec(spec)
+    x = x.contiguous()
+    in_rows, W = int(x.shape[0]), int(x.shape[1])
+    if out is None:
+        out = torch.empty((out_rows, W, 3), dtype=torch.uint8, device=x.device)
+    prm = _lib.params_from_spec(spec, policy)
+    need = _lib.lib().dfg_workspace_bytes(out_rows * W)
+    if ws is None:
+        ws = workspace(need, x.device)
+    with torch.cuda.device(x.device):
+        rc = _lib.lib().dfg_filter_rows(ctypes.c_void_p(x.data_ptr()), int(global_H), W, int(in_row0), in_rows,
+                                        x.stride(0), ctypes.c_void_p(out.data_ptr()), int(out_row0),
+                                        int(out_rows), out.stride(0), ctypes.byref(prm),
+                                        ctypes.c_void_p(ws.data_ptr()), ws.numel(),
+                                        _stream_ptr(torch, stream, x.device))
+    _lib.check(rc)
+    return out
+
+
+def filter_host(pixels_u8: np.ndarray, spec, policy=REPLICATE, out: np.ndarray | None = None,
+                stream=None) -> np.ndarray:
+    """The C ABI's host-buffer path (``dfg_filter_host``): host uint8 in,
+    host uint8 out, H2D + kernels + D2H inside one call."""
+    torch = _torch()
+    _validate_spec(spec)
+    a = np.ascontiguousarray(pixels_u8, dtype=np.uint8)
+    H, W = a.shape[:2]
+    if out is None:
+        out = np.empty_like(a)
+    prm = _lib.params_from_spec(spec, policy)
+    rc = _lib.lib().dfg_filter_host(a.ctypes.data_as(ctypes.c_void_p), H, W,
+                                    out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(prm),
+                                    _stream_ptr(torch, stream, None))
+    _lib.check(rc)
+    return out
+
+
+def last_fixup_count(device=None, stream=None) -> int:
+    """Pixels the previous call on ``device``'s cached workspace re-decided
+    in float64 (diagnostic)."""
+    torch = _torch()
+    ws = workspace(1, device)
+    cnt = ctypes.c_int64(0)
+    _lib.check(_lib.lib().dfg_fixup_count(ctypes.c_void_p(ws.data_ptr()),
+                                          _stream_ptr(torch, stream, ws.device), ctypes.byref(cnt)))
+    return int(cnt.value)
+
+
+def apply_filter(img, spec, policy=REPLICATE, workers: int = 1, *, device=None) -> RasterImage:
+    """Filter the whole image; output pixel (r, c) is the filter of the window
+    centred there, read from the original image.
+
+    Same signature and semantics as the reference.  ``workers > 1``
+    partitions the output rows into that many bands, each filtered by its own
+    ``dfg_filter_rows`` call (the reference's row-threaded path); results are
+    bit-identical to ``workers=1``.  ``device`` (keyword-only addition)
+    selects the CUDA device.
+    """
+    pixels = img.pixels if hasattr(img, "pixels") else np.asarray(img)
+    if spec.family == "identity":  # filters.py:394-395
+        return RasterImage._adopt(np.array(pixels, dtype=np.float64, copy=True))
+    _validate_spec(spec)
+    u8 = to_uint8(pixels)
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
+    M, N = u8.shape[:2]
+    x = torch.from_numpy(u8).to(dev)
+    if workers > 1 and M > 1:
+        out = torch.empty_like(x)
+        bounds = np.linspace(0, M, min(workers, M) + 1).astype(int)
+        for r0, r1 in zip(bounds[:-1], bounds[1:]):
+            if r1 > r0:
+                filter_rows_device(x, M, 0, int(r0), int(r1 - r0), spec, policy, out=out[r0:r1])
+    else:
+        out = filter_device(x, spec, policy)
+    res = out.cpu().numpy()
+    return RasterImage._adopt(res.astype(np.float64))

@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's own
+outputs (golden fixtures) and against the float64 oracle on seeded
+config-like inputs; size-independent properties at larger sizes."""
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1009_0958_b200 import (
+    REFLECT, REPLICATE, RasterImage, apply_filter, filter_batch_device, filter_device,
+    filter_host, filter_rows_device, last_fixup_count, parse_filter_spec, synth,
+)
+
+pytestmark = pytest.mark.gpu
+
+
+def _policy(name):
+    return REPLICATE if name == "replicate" else REFLECT
+
+
+def test_golden_cases_bit_exact(cuda, golden):
+    data, cases = golden
+    bad = []
+    for i, c in enumerate(cases):
+        img = RasterImage(data[f"in{i}"].astype(np.float64))
+        out = apply_filter(img, parse_filter_spec(c["spec"]), _policy(c["border"]))
+        if not (out.pixels == data[f"out{i}"]).all():
+            bad.append((i, c, int((out.pixels != data[f"out{i}"]).any(-1).sum())))
+    assert not bad, bad[:10]
+
+
+def test_acceptance_criterion4_bit_exact(cuda, golden):
+    data, _ = golden
+    torch = cuda
+    x = torch.from_numpy(data["acc_in"]).cuda()
+    for spec in ("vmf", "bvdf:exact", "ddf:exact", "acwddf:exact"):
+        got = filter_batch_device(x, parse_filter_spec(spec)).cpu().numpy()
+        assert (got == data["acc_out_" + spec.replace(":", "_")]).all(), spec
+
+
+SPECS = [
+    "vmf", "vmf:p=1", "vmf:p=3", "bvdf:exact", "bvdf:minimax", "bvdf:minimax:q=2", "bvdf:minimax:q=3",
+    "bvdf:rgb", "bvdf:rgb:p=1", "ddf:exact", "ddf:minimax", "ddf:rgb", "ddf:exact:p=1",
+    "acwddf:exact", "acwddf:minimax", "acwddf:rgb", "acwddf:exact:lambda=3:T=5",
+    "bvdf:exact:window=5", "bvdf:minimax:window=5", "bvdf:rgb:window=5", "ddf:exact:window=5",
+    "ddf:minimax:window=5", "ddf:rgb:window=5", "acwddf:exact:window=5", "acwddf:minimax:window=5",
+    "acwddf:rgb:window=5", "vmf:window=5", "ddf:exact:window=7", "bvdf:exact:window=7",
+    "bvdf:minimax:window=7", "ddf:rgb:window=7", "acwddf:exact:window=7", "vmf:window=7",
+]
+
+
+def _mismatch_report(got, want, diag):
+    bad = (got != want).any(-1)
+    nb = int(bad.sum())
+    gaps = diag["gap"][bad]
+    tm = diag["tmargin"][bad]
+    return nb, gaps, tm
+
+
+@pytest.mark.parametrize("spec", SPECS)
+@pytest.mark.parametrize("border", ["replicate", "reflect"])
+def test_against_oracle_config_like(cuda, spec, border):
+    """Seeded gradient+rectangles+noise images (SURVEY 8(d) generator), odd
+    sizes to exercise partial tiles; bit-exact against the float64 oracle."""
+    torch = cuda
+    s = parse_filter_spec(spec)
+    H, W = (150, 173) if s.window < 7 else (77, 101)
+    for seed, noise in ((11, ("uncorrelated", 0.15)), (12, ("correlated", 0.20))):
+        img = synth.noisy_image(H, W, seed, noise)
+        want = oracle.filter_image(img, s, border, diag=True)
+        got = filter_device(torch.from_numpy(img).cuda(), s, _policy(border)).cpu().numpy()
+        nb, gaps, tm = _mismatch_report(got, want["out"], want)
+        assert nb == 0, f"{spec} {border} seed {seed}: {nb} mismatches, gaps {gaps[:8]}, tmargins {tm[:8]}"
+
+
+@pytest.mark.parametrize("spec", ["bvdf:exact", "ddf:exact", "ddf:minimax:window=5", "acwddf:rgb:window=5"])
+def test_uniform_random_images(cuda, spec):
+    """Uniform random pixels cover the whole cosine domain (reference's
+    random_image, T/_synth.py:56-59)."""
+    torch = cuda
+    rng = np.random.default_rng(20240)
+    img = rng.integers(0, 256, (96, 130, 3)).astype(np.uint8)
+    s = parse_filter_spec(spec)
+    want = oracle.filter_image(img, s)
+    got = filter_device(torch.from_numpy(img).cuda(), s).cpu().numpy()
+    assert (got == want).all()
+
+
+def test_workers_and_rows_bit_identical(cuda):
+    """Row partitions (reference workers > 1, filters.py:416-430) and strips
+    with halos give the same pixels as the whole-image call."""
+    torch = cuda
+    img = synth.noisy_image(203, 97, 21, ("correlated", 0.2))
+    for spec in ("vmf", "bvdf:minimax", "acwddf:exact", "ddf:exact:window=7"):
+        s = parse_filter_spec(spec)
+        full = apply_filter(RasterImage(img.astype(np.float64)), s)
+        part = apply_filter(RasterImage(img.astype(np.float64)), s, workers=5)
+        assert full == part, spec
+        # a strip with its halo only
+        h = s.window // 2
+        x = torch.from_numpy(img).cuda()
+        r0, r1 = 50, 131
+        strip = x[r0 - h:r1 + h]
+        got = filter_rows_device(strip, img.shape[0], r0 - h, r0, r1 - r0, s).cpu().numpy()
+        assert (got == full.pixels[r0:r1]).all(), spec
+
+
+def test_batch_equals_frames(cuda):
+    torch = cuda
+    frames = np.stack([synth.noisy_image(45, 70, 1000 + i, ("uncorrelated", 0.1)) for i in range(5)])
+    s = parse_filter_spec("acwddf:exact")
+    got = filter_batch_device(torch.from_numpy(frames).cuda(), s).cpu().numpy()
+    for i in range(5):
+        want = filter_device(torch.from_numpy(frames[i]).cuda(), s).cpu().numpy()
+        assert (got[i] == want).all()
+
+
+def test_host_path_equals_device_path(cuda):
+    torch = cuda
+    img = synth.noisy_image(130, 257, 2, ("uncorrelated", 0.15))
+    s = parse_filter_spec("ddf:exact")
+    a = filter_host(img, s)
+    b = filter_device(torch.from_numpy(img).cuda(), s).cpu().numpy()
+    assert (a == b).all()
+
+
+def test_properties_at_config_size(cuda):
+    """At a BASELINE-size frame (C2: 1024^2 DDF 3x3 exact): selection
+    property (each output is a pixel of its window), determinism, and the
+    re-decision rate stays small."""
+    torch = cuda
+    img = synth.config_input("c2")
+    s = parse_filter_spec("ddf:exact")
+    x = torch.from_numpy(img).cuda()
+    a = filter_device(x, s)
+    nfix = last_fixup_count()
+    b = filter_device(x, s)
+    assert torch.equal(a, b)
+    out = a.cpu().numpy()
+    pad = np.pad(img, ((1, 1), (1, 1), (0, 0)), mode="edge")
+    member = np.zeros(img.shape[:2], bool)
+    for u in range(3):
+        for v in range(3):
+            member |= (pad[u:u + img.shape[0], v:v + img.shape[1]] == out).all(-1)
+    assert member.all()
+    assert nfix < 0.005 * img.shape[0] * img.shape[1], nfix
+
+
+def test_constant_image_fixed_point_and_idempotence(cuda):
+    img = RasterImage(np.full((37, 41, 3), 31.0))
+    for spec in ("vmf", "bvdf:minimax", "ddf:rgb", "acwddf:exact", "ddf:minimax:window=7"):
+        out = img
+        for _ in range(2):
+            out = apply_filter(out, parse_filter_spec(spec))
+        assert out == img
+
+
+def test_invalid_inputs_raise(cuda):
+    with pytest.raises(ValueError):
+        apply_filter(RasterImage(np.full((4, 4, 3), 0.5)), parse_filter_spec("vmf"))
+    with pytest.raises(ValueError):
+        apply_filter(RasterImage(np.full((4, 4, 3), 256.0)), parse_filter_spec("vmf"))
+    with pytest.raises(NotImplementedError):
+        apply_filter(RasterImage(np.full((4, 4, 3), 5.0)), parse_filter_spec("vmf:window=9"))
