@@ -4,8 +4,10 @@ Each translation unit under ``csrc/`` is compiled with nvcc
 (``-gencode arch=compute_100a,code=sm_100a -lineinfo -O3``) in parallel,
 then linked into ``paper_1009_0958_b200/libdfg.so`` (static cudart, so the
 library is self-contained and travels with the repo snapshot).  The float64
-re-decision unit is compiled with ``-fmad=false``: no contraction of
-multiply-adds, so its arithmetic rounds like the reference's.
+re-decision code is compiled with ``-fmad=false``: no contraction of
+multiply-adds, so its arithmetic rounds like the reference's.  (Applied
+to every unit: the float64 stage is inlined into the decision kernels; the
+FP32 code spells its fused multiply-adds explicitly with fmaf.)
 """
 
 from __future__ import annotations
@@ -24,9 +26,9 @@ LIB = PKG / "libdfg.so"
 INCLUDE = PKG.parent / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
+COMMON = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
           f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
-PER_FILE = {"dfg_fixup.cu": ["-fmad=false"]}
+PER_FILE: dict = {}
 
 
 def _nvcc() -> str:

@@ -35,6 +35,7 @@
 
 #include <type_traits>
 
+#include "dfg_f64.cuh"
 #include "dfg_internal.cuh"
 
 namespace dfg {
@@ -88,18 +89,17 @@ __device__ __forceinline__ Cross cross_dot(const float4 &a, const float4 &b)
     return r;
 }
 
-// Exact route: acos(a.b / |a||b|) = atan2(|a x b|, a.b), one MUFU.
+// Exact route: acos(a.b / |a||b|) = atan2(|a x b|, a.b), one MUFU.  The
+// max(.., 1e-30) makes the parallel (cc = 0 -> 0) and orthogonal
+// (dot = 0 -> pi/2) cases fall out of the same formula (m = 0).
 __device__ __forceinline__ float angle_exact(const float4 &a, const float4 &b)
 {
     const Cross x = cross_dot(a, b);
     const float dd = x.dot * x.dot;
-    const float R = rsqrt_approx(x.cc * dd);     // 1 / (|a x b| * a.b)
-    const float m = fminf(x.cc, dd) * R;         // min(tan, cot) in [0, 1]
+    const float R = rsqrt_approx(fmaxf(x.cc * dd, 1e-30f));  // 1 / (|a x b| * a.b)
+    const float m = fminf(x.cc, dd) * R;                     // min(tan, cot) in [0, 1]
     const float at = atan01(m);
-    float th = (x.cc > dd) ? (kHalfPi - at) : at;
-    th = (x.cc == 0.f) ? 0.f : th;               // parallel: exactly 0 (distance.py:173-179)
-    th = (x.dot == 0.f) ? kHalfPi : th;          // orthogonal
-    return th;
+    return (x.cc > dd) ? (kHalfPi - at) : at;
 }
 
 // Float64 replica of the reference's minimax pair (_engine.py:134-147), used
@@ -136,8 +136,8 @@ __device__ __forceinline__ float angle_minimax(const float4 &a, const float4 &b,
     float z = x.dot * rnab;
     z = fminf(fmaxf(z, 0.f), 1.f);
     // sqrt(1 - z) = |a x b| / (|a||b| sqrt(1 + z))   (Lagrange identity)
-    const float R = rsqrt_approx(x.cc * (1.f + z));
-    const float t = (x.cc == 0.f) ? 0.f : x.cc * R * rnab;
+    const float R = rsqrt_approx(fmaxf(x.cc * (1.f + z), 1e-30f));
+    const float t = x.cc * R * rnab;  // cc = 0 (parallel) -> 0
     float pa = fmaf(kp.ca[4], z, kp.ca[3]);
     pa = fmaf(pa, z, kp.ca[2]);
     pa = fmaf(pa, z, kp.ca[1]);
@@ -179,18 +179,40 @@ __device__ __forceinline__ float chroma(const float4 &a, float sa, const float4 
     return __powf(s, kp.invp);
 }
 
-template <int S, int FAM, int TH>
+// Compile-time loop: f(std::integral_constant<int, I>) for I in [B, E).
+template <int B, int E, typename F>
+__device__ __forceinline__ void static_for(F &&f)
+{
+    if constexpr (B < E) {
+        f(std::integral_constant<int, B>{});
+        static_for<B + 1, E>(f);
+    }
+}
+
+// Gray-mapped angular vector of a raw record (zero vector -> (1,1,1),
+// _engine.py:60-63); aux (1/|g| or 1/sum(g)) is carried through.
+__device__ __forceinline__ float4 gray(const float4 &r)
+{
+    const bool z = (r.x + r.y + r.z) == 0.f;
+    return make_float4(z ? 1.f : r.x, z ? 1.f : r.y, z ? 1.f : r.z, r.w);
+}
+
+// Tile geometry: 32 columns x TR thread-rows; each thread owns OPT vertically
+// adjacent output pixels (register blocking of the aggregation stage).
+template <int S, int FAM, int OPT, int TR>
 struct Cfg {
     static constexpr int H = S / 2, N = S * S, DC = (N - 1) / 2;
     static constexpr bool NEED_A = FAM != FAM_VMF;
     static constexpr bool NEED_L = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
     static constexpr bool BOTH = NEED_A && NEED_L;
-    static constexpr int TW = 32, NT = TH * TW;
+    static constexpr int TW = 32, NT = TR * TW, TH = TR * OPT;
     static constexpr int RH = TH + 2 * H, RW = TW + 2 * H, RN = RH * RW;
     static constexpr int RN4 = (RN + 3) & ~3;
     static constexpr int NDV = 2 * S - 1;
+    static constexpr int PADC = S - 1, RWS = RW + 2 * PADC;  // record rows padded for unclamped dv reads
+    static constexpr int RECN = RH * RWS;
     using DT = typename std::conditional<BOTH, float2, float>::type;
-    static constexpr size_t kSmem = (size_t)RN * 16 * 2 + (size_t)RN4 * 4 + (size_t)NDV * RN * sizeof(DT);
+    static constexpr size_t kSmem = (size_t)RECN * 16 + (size_t)RN4 * 4 + (size_t)NDV * RN * sizeof(DT);
 };
 
 __device__ __forceinline__ float dval_a(float v) { return v; }
@@ -223,43 +245,51 @@ struct Sel {
     __device__ __forceinline__ bool doubtful() const { return (v2 - v1) <= (e1 + e2); }
 };
 
-template <int S, int FAM, int ST, int PC, int TH>
-__device__ __forceinline__ typename Cfg<S, FAM, TH>::DT
-pair_value(const float4 *sA, const float4 *sX, int p, int q, const KParams &kp)
+// Distance value(s) of one pair; p/q are raw records, pg/qg gray-mapped.
+template <int FAM, int ST, int PC, typename DT>
+__device__ __forceinline__ DT pair_value(const float4 &p, const float4 &pg, const float4 &q, const float4 &qg,
+                                         const KParams &kp)
 {
-    using C = Cfg<S, FAM, TH>;
+    constexpr bool NA = FAM != FAM_VMF;
+    constexpr bool NL = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
     float da = 0.f, dl = 0.f;
-    if (C::NEED_A) {
-        const float4 a = sA[p], b = sA[q];
-        if (ST == ST_EXACT) da = angle_exact(a, b);
-        else if (ST == ST_MINIMAX) da = angle_minimax(a, b, kp);
-        else da = chroma<PC>(a, sX[p].w, b, sX[q].w, kp);
+    if (NA) {
+        if (ST == ST_EXACT) da = angle_exact(pg, qg);
+        else if (ST == ST_MINIMAX) da = angle_minimax(pg, qg, kp);
+        else da = chroma<PC>(pg, pg.x + pg.y + pg.z, qg, qg.x + qg.y + qg.z, kp);
     }
-    if (C::NEED_L) dl = minkowski<PC>(sX[p], sX[q], kp);
-    if constexpr (C::BOTH) return make_float2(da, dl);
-    else if constexpr (C::NEED_A) return da;
+    if (NL) dl = minkowski<PC>(p, q, kp);
+    if constexpr (NA && NL) return make_float2(da, dl);
+    else if constexpr (NA) return da;
     else return dl;
 }
 
-template <int S, int FAM, int ST, int PC, int TH, int MINB>
-__global__ void __launch_bounds__(TH * 32, MINB)
+template <int S, int FAM, int ST, int PC, int OPT, int TR, int MINB>
+__global__ void __launch_bounds__(TR * 32, MINB)
 dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const KParams kp)
 {
-    using C = Cfg<S, FAM, TH>;
+    using C = Cfg<S, FAM, OPT, TR>;
     using DT = typename C::DT;
-    constexpr int H = C::H, N = C::N, DC = C::DC, RW = C::RW, RH = C::RH, RN = C::RN, NT = C::NT;
+    constexpr int H = C::H, N = C::N, DC = C::DC, RW = C::RW, RH = C::RH, RN = C::RN, NT = C::NT, TH = C::TH;
+    constexpr bool ACW = FAM == FAM_ACWDDF;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float4 *sA = reinterpret_cast<float4 *>(smem_raw);
-    float4 *sX = sA + RN;
-    uint32_t *sK = reinterpret_cast<uint32_t *>(sX + RN);
-    DT *sD = reinterpret_cast<DT *>(sK + C::RN4);
+    float4 *sR = reinterpret_cast<float4 *>(smem_raw);           // raw channels + aux (padded rows)
+    uint32_t *sK = reinterpret_cast<uint32_t *>(sR + C::RECN);   // packed colour
+    DT *sD = reinterpret_cast<DT *>(sK + C::RN4);                // pair-distance planes
+    constexpr int RWS = C::RWS, PADC = C::PADC;
+
+    __shared__ unsigned s_nflag;          // this CTA's pixels needing float64 re-decision
+    __shared__ uint16_t s_flag[TH * 32];  // (window top row << 5) | column
+    __shared__ int s_b;
+    __shared__ double s_m;
 
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
     const int tile_x0 = blockIdx.x * 32, tile_y0 = blockIdx.y * TH;
     const int frame = blockIdx.z;
     const uint8_t *fin = in + (long long)frame * kp.in_fstride;
+    if (tid == 0) s_nflag = 0;
 
     // ---- stage 0: region staging + per-pixel normalisation ----------------
     for (int idx = tid; idx < RN; idx += NT) {
@@ -269,199 +299,270 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         const int gx = resolve_idx(tile_x0 + rx - H, kp.W, kp.border);
         const uint8_t *px = fin + (long long)gy * kp.in_pitch + gx * 3;
         const uint32_t r8 = px[0], g8 = px[1], b8 = px[2];
-        const float r = (float)r8, g = (float)g8, b = (float)b8;
-        const bool zero = (r8 | g8 | b8) == 0;
-        const float g1 = zero ? 1.f : r, g2 = zero ? 1.f : g, g3 = zero ? 1.f : b;
-        const float gs = g1 + g2 + g3;
+        const float4 raw = make_float4((float)r8, (float)g8, (float)b8, 0.f);
+        const float4 g = gray(raw);
         float aux = 0.f;
-        if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(g3, g3, fmaf(g2, g2, g1 * g1)));
-        if (ST == ST_CHROMA) aux = __frcp_rn(gs);
-        sA[idx] = make_float4(g1, g2, g3, aux);
-        sX[idx] = make_float4(r, g, b, gs);
+        if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(g.z, g.z, fmaf(g.y, g.y, g.x * g.x)));
+        if (ST == ST_CHROMA) aux = __frcp_rn(g.x + g.y + g.z);
+        sR[ry * RWS + PADC + rx] = make_float4(raw.x, raw.y, raw.z, aux);
         sK[idx] = r8 | (g8 << 8) | (b8 << 16);
     }
-
-    float aA[C::NEED_A ? N : 1], aL[C::NEED_L ? N : 1];
-    float AD[FAM == FAM_ACWDDF ? N : 1], LD[FAM == FAM_ACWDDF ? N : 1];
-#pragma unroll
-    for (int i = 0; i < N; i++) {
-        if (C::NEED_A) aA[i] = kp.self_term;
-        if (C::NEED_L) aL[i] = 0.f;
+    for (int idx = tid; idx < RH * 2 * PADC; idx += NT) {  // pad columns (read, never used)
+        const int ry = idx / (2 * PADC), c = idx - ry * 2 * PADC;
+        sR[ry * RWS + (c < PADC ? c : RW + c)] = make_float4(1.f, 1.f, 1.f, 1.f);
     }
-    if (FAM == FAM_ACWDDF) {
-        AD[DC] = kp.self_term;
-        LD[DC] = 0.f;
+
+    float aA[OPT][C::NEED_A ? N : 1], aL[OPT][C::NEED_L ? N : 1];
+    float AD[OPT][ACW ? N : 1], LD[OPT][ACW ? N : 1];
+#pragma unroll
+    for (int o = 0; o < OPT; o++) {
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            if (C::NEED_A) aA[o][i] = kp.self_term;
+            if (C::NEED_L) aL[o][i] = 0.f;
+        }
+        if (ACW) {
+            AD[o][DC] = kp.self_term;
+            LD[o][DC] = 0.f;
+        }
     }
     __syncthreads();
 
-#pragma unroll
-    for (int du = 0; du < S; du++) {
-        const int dv0 = (du == 0) ? 1 : -(S - 1);
-        const int ndv = S - dv0;
+    static_for<0, S>([&](auto du_c) {
+        constexpr int du = decltype(du_c)::value;
+        constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
+        constexpr int ndv = S - dv0;
         // ---- stage 1: pair distances of the region, each pair once --------
-        const int items = (RH - du) * ndv * RW;
+        // thread item = pixel p; p's record stays in registers across dv;
+        // q reads are at constant offsets (padded rows, no clamping)
+        constexpr int items = (RH - du) * RW;
         for (int it = tid; it < items; it += NT) {
-            const int px = it % RW;
-            const int rest = it / RW;
-            const int k = rest % ndv;
-            const int py = rest / ndv;
-            const int qx = min(max(px + dv0 + k, 0), RW - 1);  // out-of-region pairs: never read
-            const int p = py * RW + px, q = (py + du) * RW + qx;
-            sD[k * RN + p] = pair_value<S, FAM, ST, PC, TH>(sA, sX, p, q, kp);
+            const int py = it / RW, px = it - py * RW;
+            const float4 *prow = sR + py * RWS + PADC + px;
+            const float4 pr = prow[0];
+            const float4 pg = gray(pr);
+            const float4 *qrow = prow + du * RWS + dv0;
+#pragma unroll
+            for (int k = 0; k < ndv; k++) {
+                const float4 qr = qrow[k];
+                sD[k * RN + it] = pair_value<FAM, ST, PC, DT>(pr, pg, qr, gray(qr), kp);
+            }
         }
         __syncthreads();
         // ---- stage 2: window aggregation from the planes ------------------
+        // rows r = 0 .. S-du-1+OPT-1 below the thread's first output row feed
+        // output o's window row u = r - o.
+        const DT *dbase = sD + (ty * OPT) * RW + tx;
+        static_for<0, ndv>([&](auto k_c) {
+            constexpr int k = decltype(k_c)::value;
+            constexpr int dv = dv0 + k;
+            constexpr int vlo = dv < 0 ? -dv : 0, vhi = dv > 0 ? S - dv : S;
 #pragma unroll
-        for (int k = 0; k < ndv; k++) {
-            const int dv = dv0 + k;
-            const int vlo = dv < 0 ? -dv : 0, vhi = dv > 0 ? S - dv : S;
-#pragma unroll
-            for (int u = 0; u + du < S; u++) {
+            for (int r = 0; r < S - du + OPT - 1; r++) {
 #pragma unroll
                 for (int v = vlo; v < vhi; v++) {
-                    const int i = u * S + v, j = (u + du) * S + v + dv;
-                    const DT val = sD[k * RN + (ty + u) * RW + tx + v];
-                    if (C::NEED_A) {
-                        const float x = dval_a(val);
-                        aA[i] += x;
-                        aA[j] += x;
-                        if (FAM == FAM_ACWDDF) {
-                            if (j == DC) AD[i] = x;
-                            else if (i == DC) AD[j] = x;
+                    const DT val = dbase[k * RN + r * RW + v];
+#pragma unroll
+                    for (int o = 0; o < OPT; o++) {
+                        const int u = r - o;
+                        if (u < 0 || u + du >= S) continue;
+                        const int i = u * S + v, j = (u + du) * S + v + dv;
+                        if (C::NEED_A) {
+                            const float x = dval_a(val);
+                            aA[o][i] += x;
+                            aA[o][j] += x;
+                            if (ACW) {
+                                if (j == DC) AD[o][i] = x;
+                                else if (i == DC) AD[o][j] = x;
+                            }
                         }
-                    }
-                    if (C::NEED_L) {
-                        const float x = dval_l(val);
-                        aL[i] += x;
-                        aL[j] += x;
-                        if (FAM == FAM_ACWDDF) {
-                            if (j == DC) LD[i] = x;
-                            else if (i == DC) LD[j] = x;
+                        if (C::NEED_L) {
+                            const float x = dval_l(val);
+                            aL[o][i] += x;
+                            aL[o][j] += x;
+                            if (ACW) {
+                                if (j == DC) LD[o][i] = x;
+                                else if (i == DC) LD[o][j] = x;
+                            }
                         }
                     }
                 }
             }
-        }
+        });
         __syncthreads();
-    }
+    });
 
     // ---- stage 3: selection ------------------------------------------------
-    const int oy = tile_y0 + ty, ox = tile_x0 + tx;
-    const bool valid = (oy < kp.out_rows) && (ox < kp.W);
     const float er = kp.er, ea = kp.ea;
-    int b;
-    bool doubt;
-    if (FAM == FAM_ACWDDF) {
-        Sel sd, s0, s1, s2;
-        const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
+    const int ox = tile_x0 + tx;
 #pragma unroll
-        for (int i = 0; i < N; i++) {
-            const uint32_t col = sK[(ty + i / S) * RW + tx + i % S];
-            const float a = aA[i], l = aL[i];
-            const float pd = a * l;
-            const float a0 = fmaf(w0, AD[i], a), l0 = fmaf(w0, LD[i], l);
-            const float a1 = fmaf(w1, AD[i], a), l1 = fmaf(w1, LD[i], l);
-            const float a2 = fmaf(w2, AD[i], a), l2 = fmaf(w2, LD[i], l);
-            const float p0 = a0 * l0, p1 = a1 * l1, p2 = a2 * l2;
-            const float ed = 2.f * er * fabsf(pd) + 2.f * ea * l;
-            const float e0 = 2.f * er * fabsf(p0) + 2.f * ea * l0;
-            const float e1 = 2.f * er * fabsf(p1) + 2.f * ea * l1;
-            const float e2 = 2.f * er * fabsf(p2) + 2.f * ea * l2;
-            if (i == 0) {
-                sd.init(pd, ed, col, 0.f, 0.f);
-                s0.init(p0, e0, col, AD[i], LD[i]);
-                s1.init(p1, e1, col, AD[i], LD[i]);
-                s2.init(p2, e2, col, AD[i], LD[i]);
-            } else {
-                sd.add(pd, ed, i, col, 0.f, 0.f);
-                s0.add(p0, e0, i, col, AD[i], LD[i]);
-                s1.add(p1, e1, i, col, AD[i], LD[i]);
-                s2.add(p2, e2, i, col, AD[i], LD[i]);
+    for (int o = 0; o < OPT; o++) {
+        const int ry0 = ty * OPT + o;  // window top row in region coordinates
+        const int oy = tile_y0 + ry0;
+        const bool valid = (oy < kp.out_rows) && (ox < kp.W);
+        int b;
+        bool doubt;
+        if (ACW) {
+            Sel sd, s0, s1, s2;
+            const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                const uint32_t col = sK[(ry0 + i / S) * RW + tx + i % S];
+                const float a = aA[o][i], l = aL[o][i];
+                const float pd = a * l;
+                const float a0 = fmaf(w0, AD[o][i], a), l0 = fmaf(w0, LD[o][i], l);
+                const float a1 = fmaf(w1, AD[o][i], a), l1 = fmaf(w1, LD[o][i], l);
+                const float a2 = fmaf(w2, AD[o][i], a), l2 = fmaf(w2, LD[o][i], l);
+                const float p0 = a0 * l0, p1 = a1 * l1, p2 = a2 * l2;
+                const float ed = 2.f * er * fabsf(pd) + 2.f * ea * l;
+                const float e0 = 2.f * er * fabsf(p0) + 2.f * ea * l0;
+                const float e1 = 2.f * er * fabsf(p1) + 2.f * ea * l1;
+                const float e2 = 2.f * er * fabsf(p2) + 2.f * ea * l2;
+                if (i == 0) {
+                    sd.init(pd, ed, col, 0.f, 0.f);
+                    s0.init(p0, e0, col, AD[o][i], LD[o][i]);
+                    s1.init(p1, e1, col, AD[o][i], LD[o][i]);
+                    s2.init(p2, e2, col, AD[o][i], LD[o][i]);
+                } else {
+                    sd.add(pd, ed, i, col, 0.f, 0.f);
+                    s0.add(p0, e0, i, col, AD[o][i], LD[o][i]);
+                    s1.add(p1, e1, i, col, AD[o][i], LD[o][i]);
+                    s2.add(p2, e2, i, col, AD[o][i], LD[o][i]);
+                }
             }
-        }
-        float sv = 0.f, ld_sum = 0.f;
-        {
             float a = s0.xa;
             if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
-            sv = fmaf(a, s0.xl, sv);
+            float sv = a * s0.xl;
             a = s1.xa;
             if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
             sv = fmaf(a, s1.xl, sv);
             a = s2.xa;
             if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
             sv = fmaf(a, s2.xl, sv);
-            ld_sum = s0.xl + s1.xl + s2.xl;
-        }
-        const float es = 4.f * er * fmaxf(fabsf(sv), kp.threshold) +
-                         2.f * kp.ea_pair * (ST == ST_CHROMA ? kp.slope : 1.f) * ld_sum + 1e-6f;
-        const bool fires = sv > kp.threshold;
-        b = fires ? sd.i1 : DC;
-        doubt = s0.doubtful() || s1.doubtful() || s2.doubtful() || fabsf(sv - kp.threshold) <= es ||
-                (fires && sd.doubtful());
-    } else {
-        Sel sl;
+            const float ld_sum = s0.xl + s1.xl + s2.xl;
+            const float es = 4.f * er * fmaxf(fabsf(sv), kp.threshold) +
+                             2.f * kp.ea_pair * (ST == ST_CHROMA ? kp.slope : 1.f) * ld_sum + 1e-6f;
+            const bool fires = sv > kp.threshold;
+            b = fires ? sd.i1 : DC;
+            doubt = s0.doubtful() || s1.doubtful() || s2.doubtful() || fabsf(sv - kp.threshold) <= es ||
+                    (fires && sd.doubtful());
+        } else {
+            Sel sl;
 #pragma unroll
-        for (int i = 0; i < N; i++) {
-            const uint32_t col = sK[(ty + i / S) * RW + tx + i % S];
-            float v, e;
-            if (FAM == FAM_BVDF) {
-                v = aA[i];
-                e = er * fabsf(v) + ea;
-            } else if (FAM == FAM_VMF) {
-                v = aL[i];
-                e = er * v;
-            } else {
-                v = aA[i] * aL[i];
-                e = 2.f * er * fabsf(v) + 2.f * ea * aL[i];
+            for (int i = 0; i < N; i++) {
+                const uint32_t col = sK[(ry0 + i / S) * RW + tx + i % S];
+                float v, e;
+                if (FAM == FAM_BVDF) {
+                    v = aA[o][i];
+                    e = er * fabsf(v) + ea;
+                } else if (FAM == FAM_VMF) {
+                    v = aL[o][i];
+                    e = er * v;
+                } else {
+                    v = aA[o][i] * aL[o][i];
+                    e = 2.f * er * fabsf(v) + 2.f * ea * aL[o][i];
+                }
+                if (i == 0) sl.init(v, e, col, 0.f, 0.f);
+                else sl.add(v, e, i, col, 0.f, 0.f);
             }
-            if (i == 0) sl.init(v, e, col, 0.f, 0.f);
-            else sl.add(v, e, i, col, 0.f, 0.f);
+            b = sl.i1;
+            doubt = sl.doubtful();
         }
-        b = sl.i1;
-        doubt = sl.doubtful();
-    }
 
-    if (kp.dbg != nullptr && valid) {
-        float *d = kp.dbg + ((long long)frame * kp.out_rows * kp.W + (long long)oy * kp.W + ox) * (2 * N);
+        if (kp.dbg != nullptr && valid) {
+            float *d = kp.dbg + ((long long)frame * kp.out_rows * kp.W + (long long)oy * kp.W + ox) * (2 * N);
 #pragma unroll
-        for (int i = 0; i < N; i++) {
-            d[i] = C::NEED_A ? aA[i] : 0.f;
-            d[N + i] = C::NEED_L ? aL[i] : 0.f;
+            for (int i = 0; i < N; i++) {
+                d[i] = C::NEED_A ? aA[o][i] : 0.f;
+                d[N + i] = C::NEED_L ? aL[o][i] : 0.f;
+            }
+        }
+
+        if (valid) {
+            const uint32_t col = sK[(ry0 + b / S) * RW + tx + b % S];
+            uint8_t *op = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch + ox * 3;
+            op[0] = (uint8_t)(col & 0xff);
+            op[1] = (uint8_t)((col >> 8) & 0xff);
+            op[2] = (uint8_t)((col >> 16) & 0xff);
+        }
+
+        if (valid && doubt) {
+            const unsigned slot = atomicAdd(&s_nflag, 1u);
+            s_flag[slot] = (uint16_t)((ry0 << 5) | tx);
         }
     }
 
-    if (valid) {
-        const uint32_t col = sK[(ty + b / S) * RW + tx + b % S];
-        uint8_t *o = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch + ox * 3;
-        o[0] = (uint8_t)(col & 0xff);
-        o[1] = (uint8_t)((col >> 8) & 0xff);
-        o[2] = (uint8_t)((col >> 16) & 0xff);
-    }
-
-    // ---- re-decision list (warp-aggregated append) -------------------------
-    const bool flag = valid && doubt;
-    const unsigned mask = __ballot_sync(0xffffffffu, flag);
-    if (mask) {
-        const int leader = __ffs(mask) - 1;
-        unsigned base = 0;
-        if (tx == leader) base = atomicAdd(kp.flag_count, (unsigned)__popc(mask));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (flag) {
-            const unsigned slot = base + __popc(mask & ((1u << tx) - 1u));
-            kp.flag_list[slot] = (unsigned)(((long long)frame * kp.out_rows + oy) * kp.W + ox);
+    // ---- stage 4: float64 re-decision of this CTA's doubtful pixels ---------
+    // All threads of the CTA evaluate the window's pair table (the planes'
+    // shared memory is free now), one warp aggregates and selects; the
+    // work overlaps with other CTAs' FP32 stages on the same SM.
+    __syncthreads();
+    const unsigned nflag = s_nflag;
+    if (nflag == 0) return;
+    if (tid == 0) atomicAdd(kp.flag_count, nflag);
+    constexpr int P = N * (N - 1) / 2;
+    static_assert(N * sizeof(E64) + 2 * P * sizeof(double) <= C::NDV * C::RN * sizeof(DT),
+                  "float64 scratch must fit in the plane buffer");
+    E64 *e64 = reinterpret_cast<E64 *>(sD);
+    double *dA = reinterpret_cast<double *>(e64 + N);
+    double *dL = dA + P;
+    const FParams &fp = kp.fp;
+    for (unsigned f = 0; f < nflag; f++) {
+        const int code = s_flag[f];
+        const int ry0 = code >> 5, cx = code & 31;
+        for (int i = tid; i < N; i += NT) prep64(sR[(ry0 + i / S) * RWS + PADC + cx + i % S], ST, e64[i]);
+        __syncthreads();
+        pair_tables<false>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
+        __syncthreads();
+        if (ty == 0) {
+            double m;
+            const int bb = decide64(e64, fp, tx, dA, dL, &m);
+            if (tx == 0) { s_b = bb; s_m = m; }
         }
+        __syncthreads();
+        if (ST == ST_EXACT && C::NEED_A && s_m < fp.cr_margin) {
+            // pass 2: correctly rounded arccos (dfg_f64.cuh)
+            if (tid == 0) atomicAdd(kp.flag_count + 1, 1u);
+            pair_tables<true>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
+            __syncthreads();
+            if (ty == 0) {
+                double m;
+                const int bb = decide64(e64, fp, tx, dA, dL, &m);
+                if (tx == 0) s_b = bb;
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            const int bb = s_b;
+            const uint32_t col = sK[(ry0 + bb / S) * RW + cx + bb % S];
+            uint8_t *op = out + (long long)frame * kp.out_fstride + (long long)(tile_y0 + ry0) * kp.out_pitch +
+                          (tile_x0 + cx) * 3;
+            op[0] = (uint8_t)(col & 0xff);
+            op[1] = (uint8_t)((col >> 8) & 0xff);
+            op[2] = (uint8_t)((col >> 16) & 0xff);
+        }
+        __syncthreads();
     }
 }
+
+// Per (window, family) launch shape: OPT outputs per thread (register
+// blocking), TR thread-rows per CTA, MINB CTAs per SM.  Register-resident
+// state per output is n (BVDF/VMF), 2n (DDF) or 4n (ACWDDF) floats.
+template <int S, int FAM>
+struct Shape {
+    static constexpr int AGG = (FAM == FAM_ACWDDF ? 4 : (FAM == FAM_DDF ? 2 : 1)) * S * S;
+    static constexpr int OPT = (S >= 5 && 2 * AGG + 32 <= 131) ? 2 : 1;
+    static constexpr int NEED = OPT * AGG + 32;  // registers per thread, estimated
+    static constexpr int TR = (NEED > 128 && NEED <= 131) ? 16 : 8;
+    static constexpr int MINB = NEED <= 64 ? 4 : (NEED <= 128 ? 2 : 1);
+};
 
 template <int S, int FAM, int ST, int PC>
 cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp)
 {
-    // Tile height / occupancy per (window, family): register-resident
-    // aggregates are n (BVDF/VMF), 2n (DDF) or 4n (ACWDDF) floats.
-    constexpr int TH = 8;
-    constexpr int MINB = (FAM == FAM_ACWDDF && S >= 5) ? 1 : 2;
-    using C = Cfg<S, FAM, TH>;
-    auto kern = dfg_fast_kernel<S, FAM, ST, PC, TH, MINB>;
+    using SH = Shape<S, FAM>;
+    using C = Cfg<S, FAM, SH::OPT, SH::TR>;
+    auto kern = dfg_fast_kernel<S, FAM, ST, PC, SH::OPT, SH::TR, SH::MINB>;
     static unsigned long long configured = 0;  // per-device bit, idempotent
     int dev = 0;
     cudaGetDevice(&dev);
@@ -470,7 +571,7 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
         if (e != cudaSuccess) return e;
         configured |= 1ull << (dev & 63);
     }
-    dim3 grid((kp.W + 31) / 32, (kp.out_rows + TH - 1) / TH, kp.n_frames);
+    dim3 grid((kp.W + 31) / 32, (kp.out_rows + C::TH - 1) / C::TH, kp.n_frames);
     kern<<<grid, C::NT, C::kSmem, st>>>(in, out, kp);
     return cudaGetLastError();
 }

@@ -1,359 +1,9 @@
-// dfg_fixup.cu -- float64 re-decision of the pixels the FP32 kernel could not
-// decide with certainty (decision margin inside its error budget).
-//
-// One warp per listed pixel; lane i (and i + 32) owns window candidate i and
-// evaluates agg[i] = self + sum_{j != i, ascending j} d(min(i,j), max(i,j))
-// in IEEE binary64 with the reference's exact operation order
-// (_engine.py:46-164 planes and pair formulas, :232-314 aggregate order,
-// :317-402 selection, :451-487 ACWDDF switch).  This translation unit is
-// compiled with -fmad=false so no multiply-add is contracted: every product,
-// sum, quotient and square root rounds exactly as numba's (fastmath=False).
-//
-// The only non-IEEE-basic operation on the path is the exact route's acos
-// (glibc libm in the reference).  Pass 1 uses CUDA's acos; when a decision
-// margin of that pass is below 1e-12 relative, pass 2 recomputes with
-// cr_acos(): a double-double Newton refinement that returns the correctly
-// rounded arccos, which is what glibc returns in all but vanishingly rare
-// cases (verified against libm on CPU: tests/test_cr_acos.py).
+// dfg_fixup.cu -- host-callable probe of the double-double arccos used by the
+// float64 re-decision stage (dfg_f64.cuh), for CPU verification against a
+// high-precision reference and against glibc (tests/test_abi.py).
 #include <math.h>
 
-#include "dfg_internal.cuh"
-
-namespace dfg {
-
-// ---------------- double-double helpers (host + device) --------------------
-struct dd {
-    double hi, lo;
-};
-
-__host__ __device__ static inline dd two_sum(double a, double b)
-{
-    double s = a + b;
-    double bb = s - a;
-    double e = (a - (s - bb)) + (b - bb);
-    return {s, e};
-}
-
-__host__ __device__ static inline dd quick_two_sum(double a, double b)
-{
-    double s = a + b;
-    return {s, b - (s - a)};
-}
-
-__host__ __device__ static inline dd two_prod(double a, double b)
-{
-    double p = a * b;
-    return {p, fma(a, b, -p)};
-}
-
-__host__ __device__ static inline dd dd_add(dd a, dd b)
-{
-    dd s = two_sum(a.hi, b.hi);
-    dd t = two_sum(a.lo, b.lo);
-    s.lo += t.hi;
-    s = quick_two_sum(s.hi, s.lo);
-    s.lo += t.lo;
-    return quick_two_sum(s.hi, s.lo);
-}
-
-__host__ __device__ static inline dd dd_mul(dd a, dd b)
-{
-    dd p = two_prod(a.hi, b.hi);
-    p.lo += a.hi * b.lo + a.lo * b.hi;
-    return quick_two_sum(p.hi, p.lo);
-}
-
-// (-1)^k / (2k+1)!  as double-double (exact rationals rounded, hi + lo)
-#define DFG_SIN_TERMS 13
-__host__ __device__ static inline dd sin_coef(int k)
-{
-    switch (k) {
-    case 0: return {1.0, 0.0};
-    case 1: return {-0.16666666666666666, -9.25185853854297e-18};
-    case 2: return {0.008333333333333333, 1.1564823173178714e-19};
-    case 3: return {-0.0001984126984126984, -1.7209558293420705e-22};
-    case 4: return {2.7557319223985893e-06, -1.858393274046472e-22};
-    case 5: return {-2.505210838544172e-08, 1.448814070935912e-24};
-    case 6: return {1.6059043836821613e-10, 1.2585294588752098e-26};
-    case 7: return {-7.647163731819816e-13, -7.03872877733453e-30};
-    case 8: return {2.8114572543455206e-15, 1.6508842730861433e-31};
-    case 9: return {-8.22063524662433e-18, -2.2141894119604265e-34};
-    case 10: return {1.9572941063391263e-20, -1.3643503830087908e-36};
-    case 11: return {-3.868170170630684e-23, 8.843177655482344e-40};
-    default: return {6.446950284384474e-26, -1.9330404233703465e-42};
-    }
-}
-
-// sin(x) for |x| <= pi/6 in double-double (Taylor, truncation < 1e-32)
-__host__ __device__ static inline dd sin_dd(dd x)
-{
-    dd x2 = dd_mul(x, x);
-    dd p = sin_coef(DFG_SIN_TERMS - 1);
-    for (int k = DFG_SIN_TERMS - 2; k >= 0; k--) p = dd_add(dd_mul(p, x2), sin_coef(k));
-    return dd_mul(p, x);
-}
-
-// Correctly rounded arccos on [0, 1] (up to a ~1e-16-ulp rounding window):
-// one Newton step y = y0 + (cos y0 - z) / sin y0 from any starting value y0
-// within a few ulps, the residual evaluated in double-double without
-// cancellation: (1 - z) - 2 sin^2(y0/2) for z >= 1/2, sin(pi/2 - y0) - z else.
-__host__ __device__ static inline double cr_acos_from(double z, double y0)
-{
-    if (z >= 1.0) return 0.0;
-    const double PIO2_HI = 1.5707963267948966, PIO2_LO = 6.123233995736766e-17;
-    dd r;
-    if (z >= 0.5) {
-        dd s = sin_dd({0.5 * y0, 0.0});
-        dd s2 = dd_mul(s, s);
-        r = dd_add({1.0 - z, 0.0}, {-2.0 * s2.hi, -2.0 * s2.lo});
-    } else {
-        dd x = dd_add(two_sum(PIO2_HI, -y0), {PIO2_LO, 0.0});
-        r = dd_add(sin_dd(x), {-z, 0.0});
-    }
-    return y0 + (r.hi + r.lo) / sin(y0);
-}
-
-// ---------------- reference arithmetic in binary64 -------------------------
-struct E64 {
-    double raw[3];
-    double g[3];
-    double g4;
-};
-
-__device__ static inline void prep64(const uint8_t *px, int strategy, E64 &e)
-{
-    const double r = px[0], g = px[1], b = px[2];
-    e.raw[0] = r; e.raw[1] = g; e.raw[2] = b;
-    if (strategy == ST_CHROMA) {  // _engine.py:87-103
-        const double s = r + g + b;
-        if (s == 0.0) {
-            const double third = 1.0 / 3.0;
-            e.g[0] = e.g[1] = e.g[2] = third;
-        } else {
-            e.g[0] = r / s; e.g[1] = g / s; e.g[2] = b / s;
-        }
-        e.g4 = 0.0;
-    } else {  // _engine.py:46-72
-        double a1 = r, a2 = g, a3 = b;
-        if (a1 == 0.0 && a2 == 0.0 && a3 == 0.0) a1 = a2 = a3 = 1.0;
-        e.g[0] = a1; e.g[1] = a2; e.g[2] = a3;
-        const double nsq = a1 * a1 + a2 * a2 + a3 * a3;
-        e.g4 = (strategy == ST_MINIMAX) ? 1.0 / sqrt(nsq) : nsq;
-    }
-}
-
-__device__ static inline double clamp01(double z)
-{
-    if (z < 0.0) z = 0.0;
-    if (z > 1.0) z = 1.0;
-    return z;
-}
-
-__device__ static inline double mink64(const double *x, const double *y, double p)
-{
-    const double d1 = x[0] - y[0], d2 = x[1] - y[1], d3 = x[2] - y[2];
-    if (p == 2.0) return sqrt(d1 * d1 + d2 * d2 + d3 * d3);
-    if (p == 1.0) return fabs(d1) + fabs(d2) + fabs(d3);
-    return pow(pow(fabs(d1), p) + pow(fabs(d2), p) + pow(fabs(d3), p), 1.0 / p);
-}
-
-template <bool CR>
-__device__ static inline double pairA(const E64 &a, const E64 &b, const FParams &fp)
-{
-    if (fp.strategy == ST_EXACT) {  // _engine.py:111-119
-        const double dot = a.g[0] * b.g[0] + a.g[1] * b.g[1] + a.g[2] * b.g[2];
-        const double z = clamp01(dot / sqrt(a.g4 * b.g4));
-        const double y0 = acos(z);
-        return CR ? cr_acos_from(z, y0) : y0;
-    }
-    if (fp.strategy == ST_MINIMAX) {  // _engine.py:134-147
-        const double dot = a.g[0] * b.g[0] + a.g[1] * b.g[1] + a.g[2] * b.g[2];
-        const double z = clamp01(dot * (a.g4 * b.g4));
-        const double t = sqrt(1.0 - z);
-        const double *c = fp.ca, *s = fp.cs;
-        const double pa = c[0] + z * (c[1] + z * (c[2] + z * (c[3] + z * c[4])));
-        const double ps = s[0] + t * (s[1] + t * (s[2] + t * (s[3] + t * s[4])));
-        const double f = (z >= 0.5) ? 1.0 : 0.0;
-        return f * ps + (1.0 - f) * pa;
-    }
-    return mink64(a.g, b.g, fp.p);  // chromaticity planes, _engine.py:264-281
-}
-
-struct Cand {
-    double v;
-    int i;
-};
-
-__device__ static inline Cand warp_argmin(Cand c)
-{
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, c.v, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, c.i, off);
-        if (ov < c.v || (ov == c.v && oi < c.i)) { c.v = ov; c.i = oi; }
-    }
-    return c;
-}
-
-__device__ static inline double warp_min(double v)
-{
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
-    return v;
-}
-
-__device__ static inline bool same_col(const E64 &a, const E64 &b)
-{
-    return a.raw[0] == b.raw[0] && a.raw[1] == b.raw[1] && a.raw[2] == b.raw[2];
-}
-
-// First strict minimum over the (up to 2 per lane) candidates + relative gap
-// to the best candidate of a different colour.
-__device__ static inline Cand select64(const double v[2], int lane, int n, const E64 *e, double *gap)
-{
-    const double INF = __longlong_as_double(0x7ff0000000000000LL);
-    Cand c = {INF, 1 << 20};
-    if (lane < n) c = {v[0], lane};
-    if (lane + 32 < n && v[1] < c.v) c = {v[1], lane + 32};
-    c = warp_argmin(c);
-    double other = INF;
-    for (int s = 0; s < 2; s++) {
-        const int i = lane + 32 * s;
-        if (i < n && !same_col(e[i], e[c.i]) && v[s] < other) other = v[s];
-    }
-    other = warp_min(other);
-    const double den = fmax(fabs(c.v), fabs(other));
-    *gap = isinf(other) ? INF : (den == 0.0 ? 0.0 : (other - c.v) / den);
-    return c;
-}
-
-__device__ static inline double shfl_slot(const double v[2], int idx)
-{
-    const double a = __shfl_sync(0xffffffffu, v[0], idx & 31);
-    const double b = __shfl_sync(0xffffffffu, v[1], idx & 31);
-    return (idx >> 5) ? b : a;
-}
-
-// Decide one window; returns the chosen index and the smallest relative
-// decision margin (argmin gaps, ACWDDF threshold margin).
-template <bool CR>
-__device__ static int decide64(const E64 *e, const FParams &fp, int lane, double *margin)
-{
-    const int s = fp.window, n = s * s, dc = (n - 1) / 2;
-    const int fam = fp.family;
-    const bool needA = fam != FAM_VMF;
-    const bool needL = fam == FAM_VMF || fam == FAM_DDF || fam == FAM_ACWDDF;
-    double aA[2] = {0, 0}, aL[2] = {0, 0}, AD[2] = {0, 0}, LD[2] = {0, 0};
-    for (int sl = 0; sl < 2; sl++) {
-        const int i = lane + 32 * sl;
-        if (i >= n) continue;
-        double a = fp.self_term, l = 0.0, ad = fp.self_term, ld = 0.0;
-        for (int j = 0; j < n; j++) {
-            if (j == i) continue;
-            const int lo = i < j ? i : j, hi = i < j ? j : i;
-            if (needA) {
-                const double d = pairA<CR>(e[lo], e[hi], fp);
-                a += d;
-                if (j == dc) ad = d;
-            }
-            if (needL) {
-                const double d = mink64(e[lo].raw, e[hi].raw, fp.p);
-                l += d;
-                if (j == dc) ld = d;
-            }
-        }
-        aA[sl] = a; aL[sl] = l; AD[sl] = ad; LD[sl] = ld;
-    }
-    double g;
-    if (fam == FAM_VMF) {
-        const Cand c = select64(aL, lane, n, e, &g);
-        *margin = g;
-        return c.i;
-    }
-    if (fam == FAM_BVDF) {
-        const Cand c = select64(aA, lane, n, e, &g);
-        *margin = g;
-        return c.i;
-    }
-    double pd[2] = {aA[0] * aL[0], aA[1] * aL[1]};
-    const Cand cd = select64(pd, lane, n, e, &g);
-    if (fam == FAM_DDF) {
-        *margin = g;
-        return cd.i;
-    }
-    // ACWDDF (_engine.py:451-487): weights w_k = n - 2k + 2 - 1
-    double gmin = __longlong_as_double(0x7ff0000000000000LL), sv = 0.0;
-    for (int k = 0; k < 3; k++) {
-        const double w = (double)(n - 2 * (fp.lam + k) + 2 - 1);
-        double cw[2];
-        for (int sl = 0; sl < 2; sl++) cw[sl] = (aA[sl] + w * AD[sl]) * (aL[sl] + w * LD[sl]);
-        double gk;
-        const Cand c = select64(cw, lane, n, e, &gk);
-        gmin = fmin(gmin, gk);
-        double a = shfl_slot(AD, c.i);
-        const double l = shfl_slot(LD, c.i);
-        if (fp.strategy == ST_CHROMA) a = fp.slope * a + fp.intercept;
-        sv += a * l;
-    }
-    const bool fires = sv > fp.threshold;
-    if (fires) gmin = fmin(gmin, g);
-    const double den = fmax(fabs(sv), fabs(fp.threshold));
-    gmin = fmin(gmin, den == 0.0 ? 0.0 : fabs(sv - fp.threshold) / den);
-    *margin = gmin;
-    return fires ? cd.i : dc;
-}
-
-constexpr int kFixWarps = 8;
-
-__global__ void __launch_bounds__(kFixWarps * 32)
-dfg_fixup_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const KParams kp,
-                 const FParams fp)
-{
-    __shared__ E64 sE[kFixWarps][49];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const unsigned count = *kp.flag_count;
-    const int s = fp.window, n = s * s, h = s / 2;
-    const long long frame_px = (long long)kp.out_rows * kp.W;
-    E64 *e = sE[warp];
-    for (unsigned item = blockIdx.x * kFixWarps + warp; item < count; item += gridDim.x * kFixWarps) {
-        const unsigned pid = kp.flag_list[item];
-        const int frame = (int)(pid / frame_px);
-        const long long rem = pid - frame * frame_px;
-        const int oy = (int)(rem / kp.W), ox = (int)(rem - (long long)oy * kp.W);
-        const uint8_t *fin = in + (long long)frame * kp.in_fstride;
-        for (int i = lane; i < n; i += 32) {
-            const int u = i / s, v = i - u * s;
-            int gy = resolve_idx(kp.out_row0 + oy + u - h, kp.global_H, kp.border) - kp.in_row0;
-            gy = min(max(gy, 0), kp.in_rows - 1);
-            const int gx = resolve_idx(ox + v - h, kp.W, kp.border);
-            prep64(fin + (long long)gy * kp.in_pitch + gx * 3, fp.strategy, e[i]);
-        }
-        __syncwarp();
-        double margin;
-        int b = decide64<false>(e, fp, lane, &margin);
-        if (fp.strategy == ST_EXACT && fp.family != FAM_VMF && margin < 1e-12) b = decide64<true>(e, fp, lane, &margin);
-        if (lane == 0) {
-            uint8_t *o = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch + ox * 3;
-            o[0] = (uint8_t)e[b].raw[0];
-            o[1] = (uint8_t)e[b].raw[1];
-            o[2] = (uint8_t)e[b].raw[2];
-        }
-        __syncwarp();
-    }
-}
-
-}  // namespace dfg
-
-cudaError_t dfg_launch_fixup(const uint8_t *in, uint8_t *out, const dfg::KParams &kp,
-                             const dfg::FParams &fp, cudaStream_t st)
-{
-    const long long npx = (long long)kp.out_rows * kp.W * kp.n_frames;
-    long long blocks = (npx + dfg::kFixWarps - 1) / dfg::kFixWarps;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    if (blocks < 1) blocks = 1;
-    dfg::dfg_fixup_kernel<<<(unsigned)blocks, dfg::kFixWarps * 32, 0, st>>>(in, out, kp, fp);
-    return cudaGetLastError();
-}
+#include "dfg_f64.cuh"
 
 extern "C" DFG_API double dfg_cr_acos_host(double z, int32_t perturb_ulps)
 {

@@ -13,6 +13,16 @@ enum { FAM_VMF = 1, FAM_BVDF = 2, FAM_DDF = 3, FAM_ACWDDF = 4 };
 enum { ST_EXACT = 0, ST_MINIMAX = 1, ST_CHROMA = 2 };
 enum { PC_2 = 0, PC_1 = 1, PC_GEN = 2 };  // Minkowski order: p == 2, p == 1, general
 
+// Parameters of the float64 re-decision stage (reference constants in binary64).
+struct FParams {
+    int family, strategy, window;
+    double p, self_term;
+    double cs[5], ca[5];
+    int lam;
+    double threshold, slope, intercept;
+    double cr_margin;  // relative decision margin below which pass 2 (CR acos) runs
+};
+
 // Kernel-side parameter block, passed by value.
 struct KParams {
     // geometry (rows are global image rows; see dfg_filter_rows)
@@ -34,20 +44,11 @@ struct KParams {
     float er, ea, ea_pair;
     // float64 constants (seam recompute in the minimax route)
     double cs64[5], ca64[5];
-    // pixels needing the float64 re-decision
-    unsigned *flag_count;
-    unsigned *flag_list;
+    // float64 re-decision stage
+    FParams fp;
+    unsigned *flag_count;  // [0] pixels re-decided in float64, [1] of those needing pass 2
     // diagnostics: 2n floats per pixel (angular aggregates, Minkowski aggregates)
     float *dbg;
-};
-
-// Extra parameters of the float64 re-decision kernel.
-struct FParams {
-    int family, strategy, window;
-    double p, self_term;
-    double cs[5], ca[5];
-    int lam;
-    double threshold, slope, intercept;
 };
 
 // Border policy resolution (image.py:158-176): replicate = clamp,
@@ -83,5 +84,3 @@ DFG_DECLARE_LAUNCH(7, bvdf)
 DFG_DECLARE_LAUNCH(7, ddf)
 DFG_DECLARE_LAUNCH(7, acwddf)
 
-cudaError_t dfg_launch_fixup(const uint8_t *in, uint8_t *out, const dfg::KParams &kp,
-                             const dfg::FParams &fp, cudaStream_t st);

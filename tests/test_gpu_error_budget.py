@@ -18,14 +18,14 @@ def budget(spec):
     n = spec.window ** 2
     kind = spec.strategy.kind if spec.family != "vmf" else "exact"
     p = spec.acwddf.p if spec.family == "acwddf" else spec.p
-    er_pair, ea_pair = 6e-7, 1e-10
+    er_pair, ea_pair = 8e-7, 1e-10
     if kind == "minimax":
         er_pair, ea_pair = 1.2e-6, 8e-8
     if kind == "chromaticity":
         er_pair, ea_pair = 8e-7, 1e-9
     if p not in (1.0, 2.0):
         er_pair += 4e-6 * p
-    return 2 * (er_pair + n * 1.2e-7), 2 * n * ea_pair
+    return 1.25 * (er_pair + (n - 1) * 6e-8), 1.25 * n * ea_pair
 
 
 @pytest.mark.parametrize("spec", ["bvdf:exact", "bvdf:minimax", "bvdf:minimax:q=3", "bvdf:rgb", "ddf:exact:window=5",
