@@ -1,0 +1,90 @@
+"""CPU: the C-ABI library loads, exports every symbol include/dirfilt_gpu.h
+declares, lays out dfg_params as the header does, validates like the
+reference (no GPU needed for these paths), and its double-double arccos is
+correctly rounded."""
+
+import ctypes
+import math
+import re
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1009_0958_b200 import _lib, parse_filter_spec
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "dirfilt_gpu.h"
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    declared = re.findall(r"DFG_API\s+[\w\s\*]+?\b(dfg_\w+)\s*\(", HEADER.read_text())
+    assert declared and set(declared) == set(_lib.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.dfg_abi_version() == 1
+
+
+def test_params_layout_matches_header(tmp_path):
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "dirfilt_gpu.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(dfg_params), '
+                   'offsetof(dfg_params,p), offsetof(dfg_params,asin_c), offsetof(dfg_params,lam), '
+                   'offsetof(dfg_params,threshold), offsetof(dfg_params,intercept));return 0;}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    P = _lib.DfgParams
+    want = [ctypes.sizeof(P), P.p.offset, P.asin_c.offset, P.lam.offset, P.threshold.offset, P.intercept.offset]
+    assert got == want
+
+
+@pytest.mark.parametrize("text,code", [("vmf:window=9", _lib.DFG_E_UNSUP), ("bvdf:exact:window=11", _lib.DFG_E_UNSUP)])
+def test_unsupported_window_reported_before_any_cuda_call(text, code):
+    L = _lib.lib()
+    prm = _lib.params_from_spec(parse_filter_spec(text), "replicate")
+    rc = L.dfg_filter(ctypes.c_void_p(1), 4, 4, 12, ctypes.c_void_p(1), 12, ctypes.byref(prm), None, 0, None)
+    assert rc == code
+    assert b"window" in L.dfg_last_error()
+
+
+def test_invalid_params_rejected():
+    L = _lib.lib()
+    prm = _lib.params_from_spec(parse_filter_spec("acwddf"), "replicate")
+    prm.lam = 4  # lambda + 2 > (n+1)/2 for n = 9
+    assert L.dfg_filter(ctypes.c_void_p(1), 4, 4, 12, ctypes.c_void_p(1), 12, ctypes.byref(prm), None, 0, None) == -1
+    prm = _lib.params_from_spec(parse_filter_spec("ddf"), "replicate")
+    prm.window = 4
+    assert L.dfg_filter(ctypes.c_void_p(1), 4, 4, 12, ctypes.c_void_p(1), 12, ctypes.byref(prm), None, 0, None) == -1
+    prm = _lib.params_from_spec(parse_filter_spec("ddf"), "replicate")
+    assert L.dfg_filter(ctypes.c_void_p(1), 0, 4, 12, ctypes.c_void_p(1), 12, ctypes.byref(prm), None, 0, None) == -1
+    # strips must carry their halo rows
+    assert L.dfg_filter_rows(ctypes.c_void_p(1), 100, 4, 10, 20, 12, ctypes.c_void_p(1), 10, 20, 12,
+                             ctypes.byref(prm), None, 0, None) == -1
+
+
+def test_cr_acos_is_correctly_rounded():
+    """The float64 re-decision's arccos (dfg_f64.cuh) returns the correctly
+    rounded value from starting points several ulps off (the GPU's acos is
+    within 2 ulps); checked against a 160-bit mpmath evaluation."""
+    mpmath = pytest.importorskip("mpmath")
+    mpmath.mp.prec = 160
+    L = _lib.lib()
+    rng = np.random.default_rng(7)
+    a = rng.integers(0, 256, (3000, 3)).astype(float)
+    b = rng.integers(0, 256, (3000, 3)).astype(float)
+    a[(a == 0).all(1)] = 1
+    b[(b == 0).all(1)] = 1
+    zs = np.clip((a * b).sum(1) / np.sqrt((a * a).sum(1) * (b * b).sum(1)), 0, 1)
+    zs = np.concatenate([zs, rng.random(2000), 1 - rng.random(2000) ** 6, [0.0, 0.5, 1.0, 1 - 2**-53]])
+    glibc_off = 0
+    for z in zs:
+        z = float(z)
+        cr = float(mpmath.acos(mpmath.mpf(z)))
+        for pert in (-3, 0, 2):
+            assert L.dfg_cr_acos_host(z, pert) == cr, (z, pert)
+        glibc_off += math.acos(z) != cr
+    # glibc's acos (the reference's) is correctly rounded on all but ~0.1-0.2 %
+    assert glibc_off < 0.005 * len(zs)
