@@ -92,7 +92,8 @@ typedef struct dfg_params {
 DFG_API int dfg_abi_version(void);
 DFG_API const char *dfg_last_error(void);
 
-/* Device workspace needed to filter up to n_pixels output pixels per call. */
+/* Device workspace needed to filter up to n_pixels output pixels per call
+ * (diagnostic counters only; zero it once after allocation). */
 DFG_API size_t dfg_workspace_bytes(int64_t n_pixels);
 
 /* Whole image: d_in (H, W, 3) -> d_out (H, W, 3), both device memory. */
@@ -124,9 +125,11 @@ DFG_API int dfg_filter_batch(const uint8_t *d_in, int32_t B, int32_t H, int32_t 
 DFG_API int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out,
                     const dfg_params *prm, void *stream);
 
-/* Number of pixels the last call on this workspace re-decided in float64
- * (synchronous read of the workspace counter). */
+/* Pixels re-decided in float64 by the calls on this workspace since the last
+ * dfg_reset_counts (synchronous read of the workspace counter; the filter
+ * calls only add to it, so they need no reset launch of their own). */
 DFG_API int dfg_fixup_count(const void *d_workspace, void *stream, int64_t *count);
+DFG_API int dfg_reset_counts(void *d_workspace, void *stream);
 
 /* Diagnostics: the FP32 selection value of every window candidate
  * (n floats per pixel, window order) as the fast kernel computes them, for

@@ -14,6 +14,7 @@ from .filters import (
     filter_device,
     filter_host,
     filter_rows_device,
+    fixup_counts,
     last_fixup_count,
 )
 from .image import REFLECT, REPLICATE, BorderPolicy, ColorVector, RasterImage, to_uint8
@@ -39,5 +40,5 @@ __all__ = [
     "CALIBRATION_INTERCEPT", "CALIBRATION_SLOPE", "ColorVector", "DirectionalStrategy",
     "FAMILIES", "FastAcosTable", "FilterSpec", "MinimaxPoly", "REFLECT", "REPLICATE",
     "RasterImage", "apply_filter", "center_weight", "filter_batch_device", "filter_device",
-    "filter_host", "filter_rows_device", "last_fixup_count", "parse_filter_spec", "to_uint8",
+    "filter_host", "filter_rows_device", "fixup_counts", "last_fixup_count", "parse_filter_spec", "to_uint8",
 ]

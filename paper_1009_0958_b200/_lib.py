@@ -20,7 +20,7 @@ BORDER_CODE = {"replicate": 0, "reflect": 1}
 EXPORTS = (
     "dfg_abi_version", "dfg_last_error", "dfg_workspace_bytes", "dfg_filter",
     "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_fixup_count",
-    "dfg_debug_values", "dfg_cr_acos_host",
+    "dfg_reset_counts", "dfg_debug_values", "dfg_cr_acos_host",
 )
 
 
@@ -64,11 +64,12 @@ def lib() -> ctypes.CDLL:
     L.dfg_filter_batch.argtypes = [vp, i32, i32, i32, i64, i64, vp, i64, i64, P, vp, sz, vp]
     L.dfg_filter_host.argtypes = [vp, i32, i32, vp, P, vp]
     L.dfg_fixup_count.argtypes = [vp, vp, ctypes.POINTER(i64)]
+    L.dfg_reset_counts.argtypes = [vp, vp]
     L.dfg_debug_values.argtypes = [vp, i32, i32, i64, vp, P, vp]
     L.dfg_cr_acos_host.argtypes = [ctypes.c_double, i32]
     L.dfg_cr_acos_host.restype = ctypes.c_double
     for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host",
-                 "dfg_fixup_count", "dfg_debug_values"):
+                 "dfg_fixup_count", "dfg_reset_counts", "dfg_debug_values"):
         getattr(L, name).restype = ctypes.c_int
     if L.dfg_abi_version() != 1:
         raise RuntimeError("libdfg.so ABI version mismatch; rebuild")

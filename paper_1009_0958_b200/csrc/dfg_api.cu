@@ -183,9 +183,7 @@ int run(const uint8_t *d_in, int global_H, int W, int in_row0, int in_rows, long
     kp.flag_count = (unsigned *)ws;
     kp.dbg = dbg;
 
-    cudaError_t e = cudaMemsetAsync(kp.flag_count, 0, 2 * sizeof(unsigned), st);
-    if (e != cudaSuccess) return cuda_fail(e, "workspace reset");
-    e = launch_fast(prm, st, d_in, d_out, kp);
+    cudaError_t e = launch_fast(prm, st, d_in, d_out, kp);
     if (e != cudaSuccess) return cuda_fail(e, "fast kernel launch");
     return DFG_OK;
 }
@@ -263,6 +261,7 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
         cudaError_t e = cudaMalloc(&c.d_in, 3 * px);
         if (e == cudaSuccess) e = cudaMalloc(&c.d_out, 3 * px);
         if (e == cudaSuccess) e = cudaMalloc(&c.ws, dfg_workspace_bytes((int64_t)px));
+        if (e == cudaSuccess) e = cudaMemset(c.ws, 0, dfg_workspace_bytes((int64_t)px));
         if (e != cudaSuccess) {
             c.px_cap = 0;
             return cuda_fail(e, "device staging allocation");
@@ -293,6 +292,14 @@ int dfg_fixup_count(const void *ws, void *stream, int64_t *count)
     return DFG_OK;
 }
 
+int dfg_reset_counts(void *ws, void *stream)
+{
+    if (!ws) return fail(DFG_E_ARG, "null workspace");
+    cudaError_t e = cudaMemsetAsync(ws, 0, 2 * sizeof(unsigned), (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "counter reset");
+    return DFG_OK;
+}
+
 int dfg_debug_values(const uint8_t *d_in, int32_t H, int32_t W, int64_t in_pitch, float *d_vals,
                      const dfg_params *prm, void *stream)
 {
@@ -305,6 +312,7 @@ int dfg_debug_values(const uint8_t *d_in, int32_t H, int32_t W, int64_t in_pitch
     void *ws = nullptr;
     cudaError_t e = cudaMalloc(&tmp_out, 3 * (size_t)px);
     if (e == cudaSuccess) e = cudaMalloc(&ws, dfg_workspace_bytes(px));
+    if (e == cudaSuccess) e = cudaMemset(ws, 0, dfg_workspace_bytes(px));
     if (e != cudaSuccess) {
         if (tmp_out) cudaFree(tmp_out);
         return cuda_fail(e, "debug allocation");

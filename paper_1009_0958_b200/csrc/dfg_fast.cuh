@@ -189,16 +189,167 @@ __device__ __forceinline__ void static_for(F &&f)
     }
 }
 
-// Gray-mapped angular vector of a raw record (zero vector -> (1,1,1),
-// _engine.py:60-63); aux (1/|g| or 1/sum(g)) is carried through.
-__device__ __forceinline__ float4 gray(const float4 &r)
+// ---------------- packed f32x2 arithmetic (sm_100a FADD2/FMUL2/FFMA2) -------
+// Two pairs are evaluated per instruction: lanes (lo, hi) = pairs (k, k+1).
+struct P2 {
+    unsigned long long v;
+};
+__device__ __forceinline__ P2 pk2(float lo, float hi)
 {
-    const bool z = (r.x + r.y + r.z) == 0.f;
-    return make_float4(z ? 1.f : r.x, z ? 1.f : r.y, z ? 1.f : r.z, r.w);
+    P2 r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r.v) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ P2 bc2(float x) { return pk2(x, x); }  // broadcast (FFMA2 .F32 operand)
+__device__ __forceinline__ float lo2(P2 a)
+{
+    float l, h;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(l), "=f"(h) : "l"(a.v));
+    return l;
+}
+__device__ __forceinline__ float hi2(P2 a)
+{
+    float l, h;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(l), "=f"(h) : "l"(a.v));
+    return h;
+}
+__device__ __forceinline__ P2 add2(P2 a, P2 b)
+{
+    P2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ P2 sub2(P2 a, P2 b)
+{
+    P2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ P2 mul2(P2 a, P2 b)
+{
+    P2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r.v) : "l"(a.v), "l"(b.v));
+    return r;
+}
+__device__ __forceinline__ P2 fma2(P2 a, P2 b, P2 c)
+{
+    P2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r.v) : "l"(a.v), "l"(b.v), "l"(c.v));
+    return r;
+}
+
+// Scalar pixel p (gray-mapped g, aux) against a packed pixel pair Q = (q, q+1).
+struct Pix {
+    float x, y, z, aux;
+};
+struct Pair2 {
+    P2 x, y, z, aux;
+};
+
+// packed dot and |p x q|^2 (exact dot / cross components, as cross_dot)
+__device__ __forceinline__ void cross_dot2(const Pix &p, const Pair2 &q, P2 &dot, P2 &cc)
+{
+    dot = fma2(bc2(p.z), q.z, fma2(bc2(p.y), q.y, mul2(bc2(p.x), q.x)));
+    const P2 c1 = fma2(bc2(p.y), q.z, mul2(bc2(-p.z), q.y));
+    const P2 c2 = fma2(bc2(p.z), q.x, mul2(bc2(-p.x), q.z));
+    const P2 c3 = fma2(bc2(p.x), q.y, mul2(bc2(-p.y), q.x));
+    cc = fma2(c3, c3, fma2(c2, c2, mul2(c1, c1)));
+}
+
+__device__ __forceinline__ P2 atan01_2(P2 m)
+{
+    const P2 t = mul2(m, m);
+    P2 q = fma2(bc2(-0.0046935188584029675f), t, bc2(0.0242534838616848f));
+    q = fma2(q, t, bc2(-0.05948825553059578f));
+    q = fma2(q, t, bc2(0.09914451837539673f));
+    q = fma2(q, t, bc2(-0.14019551873207092f));
+    q = fma2(q, t, bc2(0.19969739019870758f));
+    q = fma2(q, t, bc2(-0.33331993222236633f));
+    q = fma2(q, t, bc2(0.9999998807907104f));
+    return mul2(m, q);
+}
+
+// exact route, two pairs (angle_exact per lane)
+__device__ __forceinline__ P2 angle_exact2(const Pix &p, const Pair2 &q)
+{
+    P2 dot, cc;
+    cross_dot2(p, q, dot, cc);
+    const P2 dd = mul2(dot, dot);
+    const P2 P = mul2(cc, dd);
+    const float c0 = lo2(cc), c1 = hi2(cc), d0 = lo2(dd), d1 = hi2(dd);
+    const P2 m = mul2(pk2(fminf(c0, d0), fminf(c1, d1)),
+                      pk2(rsqrt_approx(fmaxf(lo2(P), 1e-30f)), rsqrt_approx(fmaxf(hi2(P), 1e-30f))));
+    const P2 at = atan01_2(m);
+    const P2 alt = sub2(bc2(kHalfPi), at);
+    return pk2(c0 > d0 ? lo2(alt) : lo2(at), c1 > d1 ? hi2(alt) : hi2(at));
+}
+
+// minimax route, two pairs (angle_minimax per lane, incl. the seam check)
+__device__ __forceinline__ P2 angle_minimax2(const Pix &p, const Pair2 &q, const KParams &kp)
+{
+    P2 dot, cc;
+    cross_dot2(p, q, dot, cc);
+    const P2 rnab = mul2(bc2(p.aux), q.aux);
+    const P2 zr = mul2(dot, rnab);
+    const float z0 = fminf(lo2(zr), 1.f), z1 = fminf(hi2(zr), 1.f);  // dot >= 0: only the upper clamp bites
+    const P2 z = pk2(z0, z1);
+    const P2 u = mul2(cc, add2(z, bc2(1.f)));
+    const P2 R = pk2(rsqrt_approx(fmaxf(lo2(u), 1e-30f)), rsqrt_approx(fmaxf(hi2(u), 1e-30f)));
+    const P2 t = mul2(mul2(cc, R), rnab);
+    P2 pa = fma2(bc2(kp.ca[4]), z, bc2(kp.ca[3]));
+    pa = fma2(pa, z, bc2(kp.ca[2]));
+    pa = fma2(pa, z, bc2(kp.ca[1]));
+    pa = fma2(pa, z, bc2(kp.ca[0]));
+    P2 ps = fma2(bc2(kp.cs[4]), t, bc2(kp.cs[3]));
+    ps = fma2(ps, t, bc2(kp.cs[2]));
+    ps = fma2(ps, t, bc2(kp.cs[1]));
+    ps = fma2(ps, t, bc2(kp.cs[0]));
+    float r0 = z0 >= 0.5f ? lo2(ps) : lo2(pa);
+    float r1 = z1 >= 0.5f ? hi2(ps) : hi2(pa);
+    if (fabsf(z0 - 0.5f) < 4e-6f || fabsf(z1 - 0.5f) < 4e-6f) {  // rare: decide the branch like the reference
+        const float4 a = make_float4(p.x, p.y, p.z, p.aux);
+        if (fabsf(z0 - 0.5f) < 4e-6f) r0 = minimax_seam64(a, make_float4(lo2(q.x), lo2(q.y), lo2(q.z), 0.f), kp);
+        if (fabsf(z1 - 0.5f) < 4e-6f) r1 = minimax_seam64(a, make_float4(hi2(q.x), hi2(q.y), hi2(q.z), 0.f), kp);
+    }
+    return pk2(r0, r1);
+}
+
+// chromaticity route (p = 2), two pairs
+__device__ __forceinline__ P2 chroma2_l2(const Pix &p, const Pair2 &q)
+{
+    const float sp = p.x + p.y + p.z;
+    const P2 sq = add2(q.x, add2(q.y, q.z));
+    const P2 n1 = fma2(bc2(p.x), sq, mul2(bc2(-sp), q.x));
+    const P2 n2 = fma2(bc2(p.y), sq, mul2(bc2(-sp), q.y));
+    const P2 n3 = fma2(bc2(p.z), sq, mul2(bc2(-sp), q.z));
+    const P2 ss = fma2(n3, n3, fma2(n2, n2, mul2(n1, n1)));
+    return mul2(pk2(sqrt_approx(lo2(ss)), sqrt_approx(hi2(ss))), mul2(bc2(p.aux), q.aux));
+}
+
+// Minkowski p = 2 on the gray-mapped values (exact for nonzero pixels; the
+// caller repairs pairs touching a zero pixel)
+__device__ __forceinline__ P2 l2_2(const Pix &p, const Pair2 &q)
+{
+    const P2 d1 = sub2(bc2(p.x), q.x), d2 = sub2(bc2(p.y), q.y), d3 = sub2(bc2(p.z), q.z);
+    const P2 ss = fma2(d3, d3, fma2(d2, d2, mul2(d1, d1)));
+    return pk2(sqrt_approx(lo2(ss)), sqrt_approx(hi2(ss)));
+}
+
+// Zero-pixel flag: bit 0 of the stored aux word (1 ulp of aux, inside the
+// error budget; the exact route stores the bare flag).
+__device__ __forceinline__ bool zflag(float aux) { return (__float_as_uint(aux) & 1u) != 0u; }
+__device__ __forceinline__ float4 rawrec(float x, float y, float z, float aux)
+{
+    const bool zr = zflag(aux);
+    return make_float4(zr ? 0.f : x, zr ? 0.f : y, zr ? 0.f : z, aux);
 }
 
 // Tile geometry: 32 columns x TR thread-rows; each thread owns OPT vertically
 // adjacent output pixels (register blocking of the aggregation stage).
+// Records: two arrays of 16-byte elements, element c of a padded row holding
+// the pixel pair (c, c+1): A = {gx_c, gx_c+1, gy_c, gy_c+1}, B = {gz_c, gz_c+1,
+// aux_c, aux_c+1}, so a pair of horizontally adjacent partners loads with two
+// conflict-free LDS.128 straight into f32x2 operands.
 template <int S, int FAM, int OPT, int TR>
 struct Cfg {
     static constexpr int H = S / 2, N = S * S, DC = (N - 1) / 2;
@@ -209,16 +360,28 @@ struct Cfg {
     static constexpr int RH = TH + 2 * H, RW = TW + 2 * H, RN = RH * RW;
     static constexpr int RN4 = (RN + 3) & ~3;
     static constexpr int NDV = 2 * S - 1;
-    static constexpr int PADC = S - 1, RWS = RW + 2 * PADC;  // record rows padded for unclamped dv reads
+    static constexpr int PADC = S, RWS = RW + 2 * S + 1;  // padded record rows (unclamped dv reads)
     static constexpr int RECN = RH * RWS;
     using DT = typename std::conditional<BOTH, float2, float>::type;
-    static constexpr size_t kSmem = (size_t)RECN * 16 + (size_t)RN4 * 4 + (size_t)NDV * RN * sizeof(DT);
+    // Row offsets du are processed in groups of G (one barrier pair per
+    // group): small windows evaluate all U planes at once.
+    static constexpr int G = (S == 3) ? S : 1;
+    __host__ __device__ static constexpr int ndv_of(int du) { return du == 0 ? S - 1 : 2 * S - 1; }
+    __host__ __device__ static constexpr int plane_off(int du)
+    {
+        int o = 0;
+        for (int d = (du / G) * G; d < du; d++) o += ndv_of(d);
+        return o;
+    }
+    __host__ __device__ static constexpr int item_off(int du)
+    {
+        int o = 0;
+        for (int d = (du / G) * G; d < du; d++) o += (RH - d) * RW;
+        return o;
+    }
+    static constexpr int NPL = (G == S) ? plane_off(S - 1) + ndv_of(S - 1) : NDV;  // planes resident at once
+    static constexpr size_t kSmem = (size_t)RECN * 32 + (size_t)RN4 * 4 + (size_t)NPL * RN * sizeof(DT);
 };
-
-__device__ __forceinline__ float dval_a(float v) { return v; }
-__device__ __forceinline__ float dval_a(float2 v) { return v.x; }
-__device__ __forceinline__ float dval_l(float v) { return v; }
-__device__ __forceinline__ float dval_l(float2 v) { return v.y; }
 
 // One-pass first-strict-minimum with "best competitor of a different colour"
 // tracking.  Invariant: v2 = min over scanned candidates whose colour differs
@@ -245,23 +408,34 @@ struct Sel {
     __device__ __forceinline__ bool doubtful() const { return (v2 - v1) <= (e1 + e2); }
 };
 
-// Distance value(s) of one pair; p/q are raw records, pg/qg gray-mapped.
-template <int FAM, int ST, int PC, typename DT>
-__device__ __forceinline__ DT pair_value(const float4 &p, const float4 &pg, const float4 &q, const float4 &qg,
-                                         const KParams &kp)
+// Two pairs (p, q) and (p, q+1): angular and/or Minkowski distances.
+template <int FAM, int ST, int PC>
+__device__ __forceinline__ void pair_values2(const Pix &p, const Pair2 &q, const KParams &kp, P2 &da, P2 &dl)
 {
     constexpr bool NA = FAM != FAM_VMF;
     constexpr bool NL = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
-    float da = 0.f, dl = 0.f;
     if (NA) {
-        if (ST == ST_EXACT) da = angle_exact(pg, qg);
-        else if (ST == ST_MINIMAX) da = angle_minimax(pg, qg, kp);
-        else da = chroma<PC>(pg, pg.x + pg.y + pg.z, qg, qg.x + qg.y + qg.z, kp);
+        if (ST == ST_EXACT) da = angle_exact2(p, q);
+        else if (ST == ST_MINIMAX) da = angle_minimax2(p, q, kp);
+        else if (PC == PC_2) da = chroma2_l2(p, q);
+        else {
+            const float4 a = make_float4(p.x, p.y, p.z, p.aux);
+            da = pk2(chroma<PC>(a, p.x + p.y + p.z, make_float4(lo2(q.x), lo2(q.y), lo2(q.z), lo2(q.aux)),
+                                lo2(q.x) + lo2(q.y) + lo2(q.z), kp),
+                     chroma<PC>(a, p.x + p.y + p.z, make_float4(hi2(q.x), hi2(q.y), hi2(q.z), hi2(q.aux)),
+                                hi2(q.x) + hi2(q.y) + hi2(q.z), kp));
+        }
     }
-    if (NL) dl = minkowski<PC>(p, q, kp);
-    if constexpr (NA && NL) return make_float2(da, dl);
-    else if constexpr (NA) return da;
-    else return dl;
+    if (NL) {
+        const bool anyz = ((__float_as_uint(p.aux) | __float_as_uint(lo2(q.aux)) | __float_as_uint(hi2(q.aux))) & 1u);
+        if (PC == PC_2 && !anyz) {
+            dl = l2_2(p, q);
+        } else {  // zero pixels (raw 0 vs gray-mapped 1) or p != 2: per lane on raw values
+            const float4 a = rawrec(p.x, p.y, p.z, p.aux);
+            dl = pk2(minkowski<PC>(a, rawrec(lo2(q.x), lo2(q.y), lo2(q.z), lo2(q.aux)), kp),
+                     minkowski<PC>(a, rawrec(hi2(q.x), hi2(q.y), hi2(q.z), hi2(q.aux)), kp));
+        }
+    }
 }
 
 template <int S, int FAM, int ST, int PC, int OPT, int TR, int MINB>
@@ -271,14 +445,15 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     using C = Cfg<S, FAM, OPT, TR>;
     using DT = typename C::DT;
     constexpr int H = C::H, N = C::N, DC = C::DC, RW = C::RW, RH = C::RH, RN = C::RN, NT = C::NT, TH = C::TH;
+    constexpr int RWS = C::RWS, PADC = C::PADC;
     constexpr bool ACW = FAM == FAM_ACWDDF;
+    constexpr bool BOTH = C::BOTH;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    float4 *sR = reinterpret_cast<float4 *>(smem_raw);           // raw channels + aux (padded rows)
-    uint32_t *sK = reinterpret_cast<uint32_t *>(sR + C::RECN);   // packed colour
-    DT *sD = reinterpret_cast<DT *>(sK + C::RN4);                // pair-distance planes
-    constexpr int RWS = C::RWS, PADC = C::PADC;
-
+    float4 *sA = reinterpret_cast<float4 *>(smem_raw);       // {gx_c, gx_c+1, gy_c, gy_c+1}
+    float4 *sB = sA + C::RECN;                                // {gz_c, gz_c+1, aux_c, aux_c+1}
+    uint32_t *sK = reinterpret_cast<uint32_t *>(sB + C::RECN);  // packed colour (unpadded region)
+    DT *sD = reinterpret_cast<DT *>(sK + C::RN4);              // pair-distance planes
     __shared__ unsigned s_nflag;          // this CTA's pixels needing float64 re-decision
     __shared__ uint16_t s_flag[TH * 32];  // (window top row << 5) | column
     __shared__ int s_b;
@@ -292,102 +467,139 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     if (tid == 0) s_nflag = 0;
 
     // ---- stage 0: region staging + per-pixel normalisation ----------------
-    for (int idx = tid; idx < RN; idx += NT) {
-        const int ry = idx / RW, rx = idx - ry * RW;
-        int gy = resolve_idx(kp.out_row0 + tile_y0 + ry - H, kp.global_H, kp.border) - kp.in_row0;
-        gy = min(max(gy, 0), kp.in_rows - 1);
-        const int gx = resolve_idx(tile_x0 + rx - H, kp.W, kp.border);
-        const uint8_t *px = fin + (long long)gy * kp.in_pitch + gx * 3;
-        const uint32_t r8 = px[0], g8 = px[1], b8 = px[2];
-        const float4 raw = make_float4((float)r8, (float)g8, (float)b8, 0.f);
-        const float4 g = gray(raw);
-        float aux = 0.f;
-        if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(g.z, g.z, fmaf(g.y, g.y, g.x * g.x)));
-        if (ST == ST_CHROMA) aux = __frcp_rn(g.x + g.y + g.z);
-        sR[ry * RWS + PADC + rx] = make_float4(raw.x, raw.y, raw.z, aux);
-        sK[idx] = r8 | (g8 << 8) | (b8 << 16);
-    }
-    for (int idx = tid; idx < RH * 2 * PADC; idx += NT) {  // pad columns (read, never used)
-        const int ry = idx / (2 * PADC), c = idx - ry * 2 * PADC;
-        sR[ry * RWS + (c < PADC ? c : RW + c)] = make_float4(1.f, 1.f, 1.f, 1.f);
+    // Every padded record position c writes the first half of element c and
+    // the second half of element c-1; pads hold a neutral gray pixel.
+    for (int idx = tid; idx < C::RECN; idx += NT) {
+        const int ry = idx / RWS, c = idx - ry * RWS;
+        const int rx = c - PADC;
+        float gx = 1.f, gy = 1.f, gz = 1.f, aux = 0.f;
+        if (rx >= 0 && rx < RW) {
+            int gyy = resolve_idx(kp.out_row0 + tile_y0 + ry - H, kp.global_H, kp.border) - kp.in_row0;
+            gyy = min(max(gyy, 0), kp.in_rows - 1);
+            const int gxx = resolve_idx(tile_x0 + rx - H, kp.W, kp.border);
+            const uint8_t *px = fin + (long long)gyy * kp.in_pitch + gxx * 3;
+            const uint32_t r8 = px[0], g8 = px[1], b8 = px[2];
+            const bool zero = (r8 | g8 | b8) == 0;
+            gx = zero ? 1.f : (float)r8;
+            gy = zero ? 1.f : (float)g8;
+            gz = zero ? 1.f : (float)b8;
+            if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(gz, gz, fmaf(gy, gy, gx * gx)));
+            if (ST == ST_CHROMA) aux = __frcp_rn(gx + gy + gz);
+            aux = __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
+            sK[ry * RW + rx] = r8 | (g8 << 8) | (b8 << 16);
+        } else if (ST != ST_EXACT) {
+            aux = (ST == ST_MINIMAX) ? 0.57735026f : (1.f / 3.f);
+        }
+        float *ea = reinterpret_cast<float *>(sA + idx), *eb = reinterpret_cast<float *>(sB + idx);
+        ea[0] = gx; ea[2] = gy; eb[0] = gz; eb[2] = aux;
+        if (c > 0) {
+            ea[-4 + 1] = gx; ea[-4 + 3] = gy; eb[-4 + 1] = gz; eb[-4 + 3] = aux;
+        }
     }
 
-    float aA[OPT][C::NEED_A ? N : 1], aL[OPT][C::NEED_L ? N : 1];
-    float AD[OPT][ACW ? N : 1], LD[OPT][ACW ? N : 1];
+    // aggregates: BOTH -> packed (angular, Minkowski) pairs; else scalars
+    P2 ag[OPT][BOTH ? N : 1], cen[OPT][(BOTH && ACW) ? N : 1];
+    float aA[OPT][(C::NEED_A && !BOTH) ? N : 1], aL[OPT][(C::NEED_L && !BOTH) ? N : 1];
 #pragma unroll
     for (int o = 0; o < OPT; o++) {
 #pragma unroll
         for (int i = 0; i < N; i++) {
-            if (C::NEED_A) aA[o][i] = kp.self_term;
-            if (C::NEED_L) aL[o][i] = 0.f;
+            if constexpr (BOTH) ag[o][i] = pk2(kp.self_term, 0.f);
+            else if constexpr (C::NEED_A) aA[o][i] = kp.self_term;
+            else aL[o][i] = 0.f;
         }
-        if (ACW) {
-            AD[o][DC] = kp.self_term;
-            LD[o][DC] = 0.f;
-        }
+        if constexpr (ACW) cen[o][DC] = pk2(kp.self_term, 0.f);
     }
     __syncthreads();
 
-    static_for<0, S>([&](auto du_c) {
-        constexpr int du = decltype(du_c)::value;
-        constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
-        constexpr int ndv = S - dv0;
+    static_for<0, S / C::G>([&](auto g_c) {
+        constexpr int g0 = decltype(g_c)::value * C::G;
+        constexpr int total = C::item_off(g0 + C::G - 1) + (RH - (g0 + C::G - 1)) * RW;
         // ---- stage 1: pair distances of the region, each pair once --------
-        // thread item = pixel p; p's record stays in registers across dv;
-        // q reads are at constant offsets (padded rows, no clamping)
-        constexpr int items = (RH - du) * RW;
-        for (int it = tid; it < items; it += NT) {
-            const int py = it / RW, px = it - py * RW;
-            const float4 *prow = sR + py * RWS + PADC + px;
-            const float4 pr = prow[0];
-            const float4 pg = gray(pr);
-            const float4 *qrow = prow + du * RWS + dv0;
+        // thread item = pixel p (scalars in registers) for one row offset du;
+        // partners q, q+1 per packed step at constant offsets in padded rows;
+        // the items of the group's row offsets are flattened for balance
+        for (int itg = tid; itg < total; itg += NT) {
+            static_for<g0, g0 + C::G>([&](auto du_c) {
+                constexpr int du = decltype(du_c)::value;
+                constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
+                constexpr int ndv = C::ndv_of(du);
+                constexpr int NK2 = (ndv + 1) / 2;
+                constexpr int i0 = C::item_off(du), cnt = (RH - du) * RW;
+                constexpr int pl = C::plane_off(du);
+                if (C::G == 1 || (itg >= i0 && itg < i0 + cnt)) {
+                    const int it = itg - i0;
+                    const int py = it / RW, px = it - py * RW;
+                    const int pidx = py * RWS + PADC + px;
+                    const float4 a4 = sA[pidx], b4 = sB[pidx];
+                    const Pix p = {a4.x, a4.z, b4.x, b4.z};
+                    const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
+                    const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
 #pragma unroll
-            for (int k = 0; k < ndv; k++) {
-                const float4 qr = qrow[k];
-                sD[k * RN + it] = pair_value<FAM, ST, PC, DT>(pr, pg, qr, gray(qr), kp);
-            }
+                    for (int kk = 0; kk < NK2; kk++) {
+                        const ulonglong2 A2 = qa[2 * kk], B2 = qb[2 * kk];
+                        const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
+                        P2 da, dl;
+                        pair_values2<FAM, ST, PC>(p, q, kp, da, dl);
+                        const int k0 = pl + 2 * kk;
+                        const bool second = 2 * kk + 1 < ndv;
+                        if constexpr (BOTH) {
+                            sD[k0 * RN + it] = make_float2(lo2(da), lo2(dl));
+                            if (second) sD[(k0 + 1) * RN + it] = make_float2(hi2(da), hi2(dl));
+                        } else if constexpr (C::NEED_A) {
+                            sD[k0 * RN + it] = lo2(da);
+                            if (second) sD[(k0 + 1) * RN + it] = hi2(da);
+                        } else {
+                            sD[k0 * RN + it] = lo2(dl);
+                            if (second) sD[(k0 + 1) * RN + it] = hi2(dl);
+                        }
+                    }
+                }
+            });
         }
         __syncthreads();
         // ---- stage 2: window aggregation from the planes ------------------
         // rows r = 0 .. S-du-1+OPT-1 below the thread's first output row feed
         // output o's window row u = r - o.
         const DT *dbase = sD + (ty * OPT) * RW + tx;
-        static_for<0, ndv>([&](auto k_c) {
-            constexpr int k = decltype(k_c)::value;
-            constexpr int dv = dv0 + k;
-            constexpr int vlo = dv < 0 ? -dv : 0, vhi = dv > 0 ? S - dv : S;
+        static_for<g0, g0 + C::G>([&](auto du_c) {
+            constexpr int du = decltype(du_c)::value;
+            constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
+            constexpr int ndv = C::ndv_of(du);
+            constexpr int pl = C::plane_off(du);
+            static_for<0, ndv>([&](auto k_c) {
+                constexpr int k = decltype(k_c)::value;
+                constexpr int dv = dv0 + k;
+                constexpr int vlo = dv < 0 ? -dv : 0, vhi = dv > 0 ? S - dv : S;
 #pragma unroll
-            for (int r = 0; r < S - du + OPT - 1; r++) {
+                for (int r = 0; r < S - du + OPT - 1; r++) {
 #pragma unroll
-                for (int v = vlo; v < vhi; v++) {
-                    const DT val = dbase[k * RN + r * RW + v];
+                    for (int v = vlo; v < vhi; v++) {
+                        const DT val = dbase[(pl + k) * RN + r * RW + v];
 #pragma unroll
-                    for (int o = 0; o < OPT; o++) {
-                        const int u = r - o;
-                        if (u < 0 || u + du >= S) continue;
-                        const int i = u * S + v, j = (u + du) * S + v + dv;
-                        if (C::NEED_A) {
-                            const float x = dval_a(val);
-                            aA[o][i] += x;
-                            aA[o][j] += x;
-                            if (ACW) {
-                                if (j == DC) AD[o][i] = x;
-                                else if (i == DC) AD[o][j] = x;
-                            }
-                        }
-                        if (C::NEED_L) {
-                            const float x = dval_l(val);
-                            aL[o][i] += x;
-                            aL[o][j] += x;
-                            if (ACW) {
-                                if (j == DC) LD[o][i] = x;
-                                else if (i == DC) LD[o][j] = x;
+                        for (int o = 0; o < OPT; o++) {
+                            const int u = r - o;
+                            if (u < 0 || u + du >= S) continue;
+                            const int i = u * S + v, j = (u + du) * S + v + dv;
+                            if constexpr (BOTH) {
+                                const P2 x = *reinterpret_cast<const P2 *>(&val);
+                                ag[o][i] = add2(ag[o][i], x);
+                                ag[o][j] = add2(ag[o][j], x);
+                                if constexpr (ACW) {
+                                    if (j == DC) cen[o][i] = x;
+                                    else if (i == DC) cen[o][j] = x;
+                                }
+                            } else if constexpr (C::NEED_A) {
+                                aA[o][i] += val;
+                                aA[o][j] += val;
+                            } else {
+                                aL[o][i] += val;
+                                aL[o][j] += val;
                             }
                         }
                     }
                 }
-            }
+            });
         });
         __syncthreads();
     });
@@ -402,17 +614,18 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         const bool valid = (oy < kp.out_rows) && (ox < kp.W);
         int b;
         bool doubt;
-        if (ACW) {
+        if constexpr (ACW) {
             Sel sd, s0, s1, s2;
             const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
 #pragma unroll
             for (int i = 0; i < N; i++) {
                 const uint32_t col = sK[(ry0 + i / S) * RW + tx + i % S];
-                const float a = aA[o][i], l = aL[o][i];
+                const float a = lo2(ag[o][i]), l = hi2(ag[o][i]);
+                const float ad = lo2(cen[o][i]), ld = hi2(cen[o][i]);
                 const float pd = a * l;
-                const float a0 = fmaf(w0, AD[o][i], a), l0 = fmaf(w0, LD[o][i], l);
-                const float a1 = fmaf(w1, AD[o][i], a), l1 = fmaf(w1, LD[o][i], l);
-                const float a2 = fmaf(w2, AD[o][i], a), l2 = fmaf(w2, LD[o][i], l);
+                const float a0 = fmaf(w0, ad, a), l0 = fmaf(w0, ld, l);
+                const float a1 = fmaf(w1, ad, a), l1 = fmaf(w1, ld, l);
+                const float a2 = fmaf(w2, ad, a), l2 = fmaf(w2, ld, l);
                 const float p0 = a0 * l0, p1 = a1 * l1, p2 = a2 * l2;
                 const float ed = 2.f * er * fabsf(pd) + 2.f * ea * l;
                 const float e0 = 2.f * er * fabsf(p0) + 2.f * ea * l0;
@@ -420,14 +633,14 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                 const float e2 = 2.f * er * fabsf(p2) + 2.f * ea * l2;
                 if (i == 0) {
                     sd.init(pd, ed, col, 0.f, 0.f);
-                    s0.init(p0, e0, col, AD[o][i], LD[o][i]);
-                    s1.init(p1, e1, col, AD[o][i], LD[o][i]);
-                    s2.init(p2, e2, col, AD[o][i], LD[o][i]);
+                    s0.init(p0, e0, col, ad, ld);
+                    s1.init(p1, e1, col, ad, ld);
+                    s2.init(p2, e2, col, ad, ld);
                 } else {
                     sd.add(pd, ed, i, col, 0.f, 0.f);
-                    s0.add(p0, e0, i, col, AD[o][i], LD[o][i]);
-                    s1.add(p1, e1, i, col, AD[o][i], LD[o][i]);
-                    s2.add(p2, e2, i, col, AD[o][i], LD[o][i]);
+                    s0.add(p0, e0, i, col, ad, ld);
+                    s1.add(p1, e1, i, col, ad, ld);
+                    s2.add(p2, e2, i, col, ad, ld);
                 }
             }
             float a = s0.xa;
@@ -452,15 +665,16 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             for (int i = 0; i < N; i++) {
                 const uint32_t col = sK[(ry0 + i / S) * RW + tx + i % S];
                 float v, e;
-                if (FAM == FAM_BVDF) {
+                if constexpr (FAM == FAM_BVDF) {
                     v = aA[o][i];
                     e = er * fabsf(v) + ea;
-                } else if (FAM == FAM_VMF) {
+                } else if constexpr (FAM == FAM_VMF) {
                     v = aL[o][i];
                     e = er * v;
                 } else {
-                    v = aA[o][i] * aL[o][i];
-                    e = 2.f * er * fabsf(v) + 2.f * ea * aL[o][i];
+                    const float a = lo2(ag[o][i]), l = hi2(ag[o][i]);
+                    v = a * l;
+                    e = 2.f * er * fabsf(v) + 2.f * ea * l;
                 }
                 if (i == 0) sl.init(v, e, col, 0.f, 0.f);
                 else sl.add(v, e, i, col, 0.f, 0.f);
@@ -473,8 +687,13 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             float *d = kp.dbg + ((long long)frame * kp.out_rows * kp.W + (long long)oy * kp.W + ox) * (2 * N);
 #pragma unroll
             for (int i = 0; i < N; i++) {
-                d[i] = C::NEED_A ? aA[o][i] : 0.f;
-                d[N + i] = C::NEED_L ? aL[o][i] : 0.f;
+                if constexpr (BOTH) {
+                    d[i] = lo2(ag[o][i]);
+                    d[N + i] = hi2(ag[o][i]);
+                } else {
+                    d[i] = C::NEED_A ? aA[o][i] : 0.f;
+                    d[N + i] = C::NEED_L ? aL[o][i] : 0.f;
+                }
             }
         }
 
@@ -485,7 +704,6 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             op[1] = (uint8_t)((col >> 8) & 0xff);
             op[2] = (uint8_t)((col >> 16) & 0xff);
         }
-
         if (valid && doubt) {
             const unsigned slot = atomicAdd(&s_nflag, 1u);
             s_flag[slot] = (uint16_t)((ry0 << 5) | tx);
@@ -501,7 +719,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     if (nflag == 0) return;
     if (tid == 0) atomicAdd(kp.flag_count, nflag);
     constexpr int P = N * (N - 1) / 2;
-    static_assert(N * sizeof(E64) + 2 * P * sizeof(double) <= C::NDV * C::RN * sizeof(DT),
+    static_assert(N * sizeof(E64) + 2 * P * sizeof(double) <= C::NPL * C::RN * sizeof(DT),
                   "float64 scratch must fit in the plane buffer");
     E64 *e64 = reinterpret_cast<E64 *>(sD);
     double *dA = reinterpret_cast<double *>(e64 + N);
@@ -510,7 +728,11 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     for (unsigned f = 0; f < nflag; f++) {
         const int code = s_flag[f];
         const int ry0 = code >> 5, cx = code & 31;
-        for (int i = tid; i < N; i += NT) prep64(sR[(ry0 + i / S) * RWS + PADC + cx + i % S], ST, e64[i]);
+        for (int i = tid; i < N; i += NT) {
+            const uint32_t col = sK[(ry0 + i / S) * RW + cx + i % S];
+            prep64(make_float4((float)(col & 0xff), (float)((col >> 8) & 0xff), (float)((col >> 16) & 0xff), 0.f),
+                   ST, e64[i]);
+        }
         __syncthreads();
         pair_tables<false>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
         __syncthreads();
@@ -552,9 +774,15 @@ template <int S, int FAM>
 struct Shape {
     static constexpr int AGG = (FAM == FAM_ACWDDF ? 4 : (FAM == FAM_DDF ? 2 : 1)) * S * S;
     static constexpr int OPT = (S >= 5 && 2 * AGG + 32 <= 131) ? 2 : 1;
-    static constexpr int NEED = OPT * AGG + 32;  // registers per thread, estimated
-    static constexpr int TR = (NEED > 128 && NEED <= 131) ? 16 : 8;
-    static constexpr int MINB = NEED <= 64 ? 4 : (NEED <= 128 ? 2 : 1);
+    static constexpr int REG = OPT * AGG + 56;  // registers per thread, estimated (aggregates + working set)
+    // The register file is split per SM sub-partition (16K registers each),
+    // so the bound is warps per sub-partition, not per SM.
+    static constexpr int WPS = 16384 / (REG * 32);
+    static constexpr int TR = WPS >= 4 ? 8 : 4 * (WPS < 2 ? 2 : WPS);
+    static constexpr int MINB0 = WPS >= 4 ? (WPS / 2 > 4 ? 4 : WPS / 2) : 1;
+    // 3x3 BVDF/DDF/VMF: 4 CTAs (32 warps) per SM hide the staging and
+    // barrier latency better than the few extra registers would
+    static constexpr int MINB = (S == 3 && FAM != FAM_ACWDDF) ? 4 : MINB0;
 };
 
 template <int S, int FAM, int ST, int PC>

@@ -65,7 +65,7 @@ def workspace(nbytes: int, device=None):
     with _ws_lock:
         buf = _ws_cache.get(dev.index)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
+            buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
             _ws_cache[dev.index] = buf
         return buf
 
@@ -166,15 +166,23 @@ def filter_host(pixels_u8: np.ndarray, spec, policy=REPLICATE, out: np.ndarray |
     return out
 
 
-def last_fixup_count(device=None, stream=None) -> int:
-    """Pixels the previous call on ``device``'s cached workspace re-decided
-    in float64 (diagnostic)."""
+def fixup_counts(device=None, stream=None, reset: bool = False):
+    """(pixels re-decided in float64, of which needed the correctly rounded
+    arccos pass) accumulated on ``device``'s cached workspace since the last
+    reset (diagnostic; ``reset=True`` zeroes the counters after reading)."""
     torch = _torch()
     ws = workspace(1, device)
-    cnt = ctypes.c_int64(0)
-    _lib.check(_lib.lib().dfg_fixup_count(ctypes.c_void_p(ws.data_ptr()),
-                                          _stream_ptr(torch, stream, ws.device), ctypes.byref(cnt)))
-    return int(cnt.value)
+    counts = ws[:8].view(torch.int32).cpu().tolist()
+    if reset:
+        _lib.check(_lib.lib().dfg_reset_counts(ctypes.c_void_p(ws.data_ptr()),
+                                               _stream_ptr(torch, stream, ws.device)))
+        torch.cuda.synchronize(ws.device)
+    return counts[0], counts[1]
+
+
+def last_fixup_count(device=None, stream=None) -> int:
+    """Float64 re-decisions since the previous call (resets the counter)."""
+    return fixup_counts(device, stream, reset=True)[0]
 
 
 def apply_filter(img, spec, policy=REPLICATE, workers: int = 1, *, device=None) -> RasterImage:
