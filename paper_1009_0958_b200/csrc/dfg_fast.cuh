@@ -386,30 +386,36 @@ struct Cfg {
 // One-pass first-strict-minimum with "best competitor of a different colour"
 // tracking.  Invariant: v2 = min over scanned candidates whose colour differs
 // from the current winner's (the candidates that could change the output).
+// The error bound of a candidate, er*|v| + ea*l (l = its Minkowski factor),
+// is formed only for the two tracked candidates at the end.
 struct Sel {
-    float v1, e1, v2, e2;
+    float v1, l1, v2, l2;
     int i1;
     uint32_t k1;
     float xa, xl;  // payload of the winner (ACWDDF centre distances)
-    __device__ __forceinline__ void init(float v, float e, uint32_t k, float pa, float pl)
+    __device__ __forceinline__ void init(float v, float l, uint32_t k, float pa, float pl)
     {
-        v1 = v; e1 = e; v2 = __int_as_float(0x7f800000); e2 = 0.f; i1 = 0; k1 = k; xa = pa; xl = pl;
+        v1 = v; l1 = l; v2 = __int_as_float(0x7f800000); l2 = 0.f; i1 = 0; k1 = k; xa = pa; xl = pl;
     }
-    __device__ __forceinline__ void add(float v, float e, int i, uint32_t k, float pa, float pl)
+    __device__ __forceinline__ void add(float v, float l, int i, uint32_t k, float pa, float pl)
     {
         if (v < v1) {
-            if (k != k1) { v2 = v1; e2 = e1; }
-            v1 = v; e1 = e; i1 = i; k1 = k; xa = pa; xl = pl;
+            if (k != k1) { v2 = v1; l2 = l1; }
+            v1 = v; l1 = l; i1 = i; k1 = k; xa = pa; xl = pl;
         } else if (k != k1 && v < v2) {
-            v2 = v; e2 = e;
+            v2 = v; l2 = l;
         }
     }
     // true when the FP32 order of winner and competitor is not certain
-    __device__ __forceinline__ bool doubtful() const { return (v2 - v1) <= (e1 + e2); }
+    __device__ __forceinline__ bool doubtful(float er, float ea) const
+    {
+        // (no competitor: v2 = inf -> inf - inf = NaN -> false)
+        return (v2 - v1) - er * fabsf(v2) <= er * fabsf(v1) + ea * (l1 + l2);
+    }
 };
 
 // Two pairs (p, q) and (p, q+1): angular and/or Minkowski distances.
-template <int FAM, int ST, int PC>
+template <int FAM, int ST, int PC, bool ZC>
 __device__ __forceinline__ void pair_values2(const Pix &p, const Pair2 &q, const KParams &kp, P2 &da, P2 &dl)
 {
     constexpr bool NA = FAM != FAM_VMF;
@@ -427,7 +433,8 @@ __device__ __forceinline__ void pair_values2(const Pix &p, const Pair2 &q, const
         }
     }
     if (NL) {
-        const bool anyz = ((__float_as_uint(p.aux) | __float_as_uint(lo2(q.aux)) | __float_as_uint(hi2(q.aux))) & 1u);
+        const bool anyz =
+            ZC && ((__float_as_uint(p.aux) | __float_as_uint(lo2(q.aux)) | __float_as_uint(hi2(q.aux))) & 1u);
         if (PC == PC_2 && !anyz) {
             dl = l2_2(p, q);
         } else {  // zero pixels (raw 0 vs gray-mapped 1) or p != 2: per lane on raw values
@@ -467,35 +474,55 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     if (tid == 0) s_nflag = 0;
 
     // ---- stage 0: region staging + per-pixel normalisation ----------------
-    // Every padded record position c writes the first half of element c and
-    // the second half of element c-1; pads hold a neutral gray pixel.
-    for (int idx = tid; idx < C::RECN; idx += NT) {
-        const int ry = idx / RWS, c = idx - ry * RWS;
-        const int rx = c - PADC;
-        float gx = 1.f, gy = 1.f, gz = 1.f, aux = 0.f;
-        if (rx >= 0 && rx < RW) {
-            int gyy = resolve_idx(kp.out_row0 + tile_y0 + ry - H, kp.global_H, kp.border) - kp.in_row0;
-            gyy = min(max(gyy, 0), kp.in_rows - 1);
-            const int gxx = resolve_idx(tile_x0 + rx - H, kp.W, kp.border);
-            const uint8_t *px = fin + (long long)gyy * kp.in_pitch + gxx * 3;
-            const uint32_t r8 = px[0], g8 = px[1], b8 = px[2];
-            const bool zero = (r8 | g8 | b8) == 0;
-            gx = zero ? 1.f : (float)r8;
-            gy = zero ? 1.f : (float)g8;
-            gz = zero ? 1.f : (float)b8;
-            if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(gz, gz, fmaf(gy, gy, gx * gx)));
-            if (ST == ST_CHROMA) aux = __frcp_rn(gx + gy + gz);
-            aux = __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
-            sK[ry * RW + rx] = r8 | (g8 << 8) | (b8 << 16);
-        } else if (ST != ST_EXACT) {
-            aux = (ST == ST_MINIMAX) ? 0.57735026f : (1.f / 3.f);
-        }
-        float *ea = reinterpret_cast<float *>(sA + idx), *eb = reinterpret_cast<float *>(sB + idx);
+    // Record position c writes the first half of element c and the second
+    // half of element c-1.  Pad positions hold a neutral gray pixel; tiles
+    // whose region lies inside the image skip the border resolution.
+    auto put = [&](int pos, float gx, float gy, float gz, float aux, bool has_prev) {
+        float *ea = reinterpret_cast<float *>(sA + pos), *eb = reinterpret_cast<float *>(sB + pos);
         ea[0] = gx; ea[2] = gy; eb[0] = gz; eb[2] = aux;
-        if (c > 0) {
+        if (has_prev) {
             ea[-4 + 1] = gx; ea[-4 + 3] = gy; eb[-4 + 1] = gz; eb[-4 + 3] = aux;
         }
+    };
+    {
+        constexpr int NPAD = RWS - RW;
+        const float pad_aux = (ST == ST_MINIMAX) ? 0.57735026f : (ST == ST_CHROMA ? (1.f / 3.f) : 0.f);
+        for (int idx = tid; idx < RH * NPAD; idx += NT) {
+            const int ry = idx / NPAD, k = idx - ry * NPAD;
+            const int c = k < PADC ? k : RW + k;
+            put(ry * RWS + c, 1.f, 1.f, 1.f, pad_aux, c > 0);
+        }
     }
+    const int gy_top = kp.out_row0 + tile_y0 - H;  // global row of region row 0
+    const bool inside = gy_top >= kp.in_row0 && gy_top + RH <= kp.in_row0 + kp.in_rows &&
+                        gy_top >= 0 && gy_top + RH <= kp.global_H && tile_x0 - H >= 0 && tile_x0 - H + RW <= kp.W;
+    bool any_zero = false;
+    for (int idx = tid; idx < RN; idx += NT) {
+        const int ry = idx / RW, rx = idx - ry * RW;
+        int gyy, gxx;
+        if (inside) {
+            gyy = gy_top + ry - kp.in_row0;
+            gxx = tile_x0 - H + rx;
+        } else {
+            gyy = resolve_idx(gy_top + ry, kp.global_H, kp.border) - kp.in_row0;
+            gyy = min(max(gyy, 0), kp.in_rows - 1);
+            gxx = resolve_idx(tile_x0 + rx - H, kp.W, kp.border);
+        }
+        const uint8_t *px = fin + (long long)gyy * kp.in_pitch + gxx * 3;
+        const uint32_t r8 = px[0], g8 = px[1], b8 = px[2];
+        const bool zero = (r8 | g8 | b8) == 0;
+        any_zero |= zero;
+        const float gx = zero ? 1.f : (float)r8, gy = zero ? 1.f : (float)g8, gz = zero ? 1.f : (float)b8;
+        float aux = 0.f;
+        if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(gz, gz, fmaf(gy, gy, gx * gx)));
+        if (ST == ST_CHROMA) aux = __frcp_rn(gx + gy + gz);
+        aux = __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
+        sK[idx] = r8 | (g8 << 8) | (b8 << 16);
+        put(ry * RWS + PADC + rx, gx, gy, gz, aux, true);
+    }
+    // zero vectors (raw 0 vs gray-mapped 1) only matter to the Minkowski term
+    const bool zany = __syncthreads_or(any_zero);  // also the staging barrier
+    const bool zchk = C::NEED_L && zany;
 
     // aggregates: BOTH -> packed (angular, Minkowski) pairs; else scalars
     P2 ag[OPT][BOTH ? N : 1], cen[OPT][(BOTH && ACW) ? N : 1];
@@ -510,7 +537,6 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         }
         if constexpr (ACW) cen[o][DC] = pk2(kp.self_term, 0.f);
     }
-    __syncthreads();
 
     static_for<0, S / C::G>([&](auto g_c) {
         constexpr int g0 = decltype(g_c)::value * C::G;
@@ -519,44 +545,49 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         // thread item = pixel p (scalars in registers) for one row offset du;
         // partners q, q+1 per packed step at constant offsets in padded rows;
         // the items of the group's row offsets are flattened for balance
-        for (int itg = tid; itg < total; itg += NT) {
-            static_for<g0, g0 + C::G>([&](auto du_c) {
-                constexpr int du = decltype(du_c)::value;
-                constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
-                constexpr int ndv = C::ndv_of(du);
-                constexpr int NK2 = (ndv + 1) / 2;
-                constexpr int i0 = C::item_off(du), cnt = (RH - du) * RW;
-                constexpr int pl = C::plane_off(du);
-                if (C::G == 1 || (itg >= i0 && itg < i0 + cnt)) {
-                    const int it = itg - i0;
-                    const int py = it / RW, px = it - py * RW;
-                    const int pidx = py * RWS + PADC + px;
-                    const float4 a4 = sA[pidx], b4 = sB[pidx];
-                    const Pix p = {a4.x, a4.z, b4.x, b4.z};
-                    const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
-                    const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
-#pragma unroll
-                    for (int kk = 0; kk < NK2; kk++) {
-                        const ulonglong2 A2 = qa[2 * kk], B2 = qb[2 * kk];
-                        const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
-                        P2 da, dl;
-                        pair_values2<FAM, ST, PC>(p, q, kp, da, dl);
-                        const int k0 = pl + 2 * kk;
-                        const bool second = 2 * kk + 1 < ndv;
-                        if constexpr (BOTH) {
-                            sD[k0 * RN + it] = make_float2(lo2(da), lo2(dl));
-                            if (second) sD[(k0 + 1) * RN + it] = make_float2(hi2(da), hi2(dl));
-                        } else if constexpr (C::NEED_A) {
-                            sD[k0 * RN + it] = lo2(da);
-                            if (second) sD[(k0 + 1) * RN + it] = hi2(da);
-                        } else {
-                            sD[k0 * RN + it] = lo2(dl);
-                            if (second) sD[(k0 + 1) * RN + it] = hi2(dl);
+        auto stage1 = [&](auto zc_c) {
+            constexpr bool ZC = decltype(zc_c)::value;
+            for (int itg = tid; itg < total; itg += NT) {
+                static_for<g0, g0 + C::G>([&](auto du_c) {
+                    constexpr int du = decltype(du_c)::value;
+                    constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
+                    constexpr int ndv = C::ndv_of(du);
+                    constexpr int NK2 = (ndv + 1) / 2;
+                    constexpr int i0 = C::item_off(du), cnt = (RH - du) * RW;
+                    constexpr int pl = C::plane_off(du);
+                    if (C::G == 1 || (itg >= i0 && itg < i0 + cnt)) {
+                        const int it = itg - i0;
+                        const int py = it / RW, px = it - py * RW;
+                        const int pidx = py * RWS + PADC + px;
+                        const float4 a4 = sA[pidx], b4 = sB[pidx];
+                        const Pix p = {a4.x, a4.z, b4.x, b4.z};
+                        const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
+                        const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
+    #pragma unroll
+                        for (int kk = 0; kk < NK2; kk++) {
+                            const ulonglong2 A2 = qa[2 * kk], B2 = qb[2 * kk];
+                            const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
+                            P2 da, dl;
+                            pair_values2<FAM, ST, PC, ZC>(p, q, kp, da, dl);
+                            const int k0 = pl + 2 * kk;
+                            const bool second = 2 * kk + 1 < ndv;
+                            if constexpr (BOTH) {
+                                sD[k0 * RN + it] = make_float2(lo2(da), lo2(dl));
+                                if (second) sD[(k0 + 1) * RN + it] = make_float2(hi2(da), hi2(dl));
+                            } else if constexpr (C::NEED_A) {
+                                sD[k0 * RN + it] = lo2(da);
+                                if (second) sD[(k0 + 1) * RN + it] = hi2(da);
+                            } else {
+                                sD[k0 * RN + it] = lo2(dl);
+                                if (second) sD[(k0 + 1) * RN + it] = hi2(dl);
+                            }
                         }
                     }
-                }
-            });
-        }
+                });
+            }
+        };
+        if (zchk) stage1(std::true_type{});
+        else stage1(std::false_type{});
         __syncthreads();
         // ---- stage 2: window aggregation from the planes ------------------
         // rows r = 0 .. S-du-1+OPT-1 below the thread's first output row feed
@@ -623,24 +654,18 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                 const float a = lo2(ag[o][i]), l = hi2(ag[o][i]);
                 const float ad = lo2(cen[o][i]), ld = hi2(cen[o][i]);
                 const float pd = a * l;
-                const float a0 = fmaf(w0, ad, a), l0 = fmaf(w0, ld, l);
-                const float a1 = fmaf(w1, ad, a), l1 = fmaf(w1, ld, l);
-                const float a2 = fmaf(w2, ad, a), l2 = fmaf(w2, ld, l);
-                const float p0 = a0 * l0, p1 = a1 * l1, p2 = a2 * l2;
-                const float ed = 2.f * er * fabsf(pd) + 2.f * ea * l;
-                const float e0 = 2.f * er * fabsf(p0) + 2.f * ea * l0;
-                const float e1 = 2.f * er * fabsf(p1) + 2.f * ea * l1;
-                const float e2 = 2.f * er * fabsf(p2) + 2.f * ea * l2;
+                const float l0 = fmaf(w0, ld, l), l1 = fmaf(w1, ld, l), l2 = fmaf(w2, ld, l);
+                const float p0 = fmaf(w0, ad, a) * l0, p1 = fmaf(w1, ad, a) * l1, p2 = fmaf(w2, ad, a) * l2;
                 if (i == 0) {
-                    sd.init(pd, ed, col, 0.f, 0.f);
-                    s0.init(p0, e0, col, ad, ld);
-                    s1.init(p1, e1, col, ad, ld);
-                    s2.init(p2, e2, col, ad, ld);
+                    sd.init(pd, l, col, 0.f, 0.f);
+                    s0.init(p0, l0, col, ad, ld);
+                    s1.init(p1, l1, col, ad, ld);
+                    s2.init(p2, l2, col, ad, ld);
                 } else {
-                    sd.add(pd, ed, i, col, 0.f, 0.f);
-                    s0.add(p0, e0, i, col, ad, ld);
-                    s1.add(p1, e1, i, col, ad, ld);
-                    s2.add(p2, e2, i, col, ad, ld);
+                    sd.add(pd, l, i, col, 0.f, 0.f);
+                    s0.add(p0, l0, i, col, ad, ld);
+                    s1.add(p1, l1, i, col, ad, ld);
+                    s2.add(p2, l2, i, col, ad, ld);
                 }
             }
             float a = s0.xa;
@@ -657,30 +682,31 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                              2.f * kp.ea_pair * (ST == ST_CHROMA ? kp.slope : 1.f) * ld_sum + 1e-6f;
             const bool fires = sv > kp.threshold;
             b = fires ? sd.i1 : DC;
-            doubt = s0.doubtful() || s1.doubtful() || s2.doubtful() || fabsf(sv - kp.threshold) <= es ||
-                    (fires && sd.doubtful());
+            const float er2 = 2.f * er, ea2 = 2.f * ea;
+            doubt = s0.doubtful(er2, ea2) || s1.doubtful(er2, ea2) || s2.doubtful(er2, ea2) ||
+                    fabsf(sv - kp.threshold) <= es || (fires && sd.doubtful(er2, ea2));
         } else {
+            // BVDF: bound er|v| + ea (l = 1); VMF: er v (l = 0); DDF: 2er|v| + 2ea l
             Sel sl;
 #pragma unroll
             for (int i = 0; i < N; i++) {
                 const uint32_t col = sK[(ry0 + i / S) * RW + tx + i % S];
-                float v, e;
+                float v, l;
                 if constexpr (FAM == FAM_BVDF) {
                     v = aA[o][i];
-                    e = er * fabsf(v) + ea;
+                    l = 1.f;
                 } else if constexpr (FAM == FAM_VMF) {
                     v = aL[o][i];
-                    e = er * v;
+                    l = 0.f;
                 } else {
-                    const float a = lo2(ag[o][i]), l = hi2(ag[o][i]);
-                    v = a * l;
-                    e = 2.f * er * fabsf(v) + 2.f * ea * l;
+                    l = hi2(ag[o][i]);
+                    v = lo2(ag[o][i]) * l;
                 }
-                if (i == 0) sl.init(v, e, col, 0.f, 0.f);
-                else sl.add(v, e, i, col, 0.f, 0.f);
+                if (i == 0) sl.init(v, l, col, 0.f, 0.f);
+                else sl.add(v, l, i, col, 0.f, 0.f);
             }
             b = sl.i1;
-            doubt = sl.doubtful();
+            doubt = (FAM == FAM_DDF) ? sl.doubtful(2.f * er, 2.f * ea) : sl.doubtful(er, ea);
         }
 
         if (kp.dbg != nullptr && valid) {
@@ -778,11 +804,12 @@ struct Shape {
     // The register file is split per SM sub-partition (16K registers each),
     // so the bound is warps per sub-partition, not per SM.
     static constexpr int WPS = 16384 / (REG * 32);
-    static constexpr int TR = WPS >= 4 ? 8 : 4 * (WPS < 2 ? 2 : WPS);
+    static constexpr int TR0 = WPS >= 4 ? 8 : 4 * (WPS < 2 ? 2 : WPS);
+    static constexpr int TR = (S == 3 && FAM != FAM_ACWDDF) ? 16 : TR0;  // 16 warps x 2 CTAs, 64 registers
     static constexpr int MINB0 = WPS >= 4 ? (WPS / 2 > 4 ? 4 : WPS / 2) : 1;
     // 3x3 BVDF/DDF/VMF: 4 CTAs (32 warps) per SM hide the staging and
     // barrier latency better than the few extra registers would
-    static constexpr int MINB = (S == 3 && FAM != FAM_ACWDDF) ? 4 : MINB0;
+    static constexpr int MINB = (S == 3 && FAM != FAM_ACWDDF) ? 2 : MINB0;
 };
 
 template <int S, int FAM, int ST, int PC>
