@@ -188,17 +188,25 @@ int run(const uint8_t *d_in, int global_H, int W, int in_row0, int in_rows, long
     return DFG_OK;
 }
 
+constexpr int kMaxBands = 8;
+
 struct HostCache {
     uint8_t *d_in = nullptr, *d_out = nullptr;
     void *ws = nullptr;
     size_t px_cap = 0;
     int dev = -1;
-    ~HostCache()
+    cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams (H2D / D2H engines)
+    cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_in[kMaxBands] = {}, ev_k[kMaxBands] = {};
+    void release()
     {
         if (d_in) cudaFree(d_in);
         if (d_out) cudaFree(d_out);
         if (ws) cudaFree(ws);
+        d_in = d_out = nullptr;
+        ws = nullptr;
+        px_cap = 0;
     }
+    ~HostCache() { release(); }
 };
 thread_local HostCache g_host;
 
@@ -253,30 +261,73 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
     const size_t px = (size_t)H * W;
     cudaStream_t st = (cudaStream_t)stream;
     if (c.dev != dev || c.px_cap < px) {
-        if (c.d_in) cudaFree(c.d_in);
-        if (c.d_out) cudaFree(c.d_out);
-        if (c.ws) cudaFree(c.ws);
-        c.d_in = c.d_out = nullptr;
-        c.ws = nullptr;
+        c.release();
         cudaError_t e = cudaMalloc(&c.d_in, 3 * px);
         if (e == cudaSuccess) e = cudaMalloc(&c.d_out, 3 * px);
         if (e == cudaSuccess) e = cudaMalloc(&c.ws, dfg_workspace_bytes((int64_t)px));
         if (e == cudaSuccess) e = cudaMemset(c.ws, 0, dfg_workspace_bytes((int64_t)px));
+        if (e == cudaSuccess && c.dev != dev) {
+            e = cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_done, cudaEventDisableTiming);
+            for (int k = 0; k < kMaxBands && e == cudaSuccess; k++) {
+                e = cudaEventCreateWithFlags(&c.ev_in[k], cudaEventDisableTiming);
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_k[k], cudaEventDisableTiming);
+            }
+        }
         if (e != cudaSuccess) {
-            c.px_cap = 0;
+            c.release();
             return cuda_fail(e, "device staging allocation");
         }
         c.px_cap = px;
         c.dev = dev;
     }
-    cudaError_t e = cudaMemcpyAsync(c.d_in, h_in, 3 * px, cudaMemcpyHostToDevice, st);
+    // Row-band pipeline: H2D of band k+1 (copy engine 1), the kernel of band
+    // k (on `stream`) and D2H of band k-1 (copy engine 2) overlap.  Band k's
+    // kernel waits for the input rows its windows reach (k+1's first rows).
+    const int h = (prm->family == DFG_IDENTITY) ? 0 : prm->window / 2;
+    static const int nb_env = [] {
+        const char *s = getenv("DFG_HOST_BANDS");  // diagnostics only
+        return s ? atoi(s) : 0;
+    }();
+    // each band costs ~25 us of API calls: bands only pay off when the
+    // copies they hide are larger than that (>= ~0.5 M pixels per band)
+    int nb = nb_env > 0 ? nb_env : (int)(px / (512 * 1024));
+    if (nb > H / 64) nb = H / 64;
+    nb = nb < 1 ? 1 : (nb > kMaxBands ? kMaxBands : nb);
+    if (prm->border == DFG_REFLECT && H <= 4 * h) nb = 1;
+    const long long pitch = 3LL * W;
+    auto row0 = [&](int k) { return (int)((long long)k * H / nb); };
+    cudaError_t e = cudaEventRecord(c.ev_start, st);  // buffers are free once prior work on `stream` is done
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_in, c.ev_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_out, c.ev_start, 0);
+    for (int k = 0; k < nb && e == cudaSuccess; k++) {
+        const int r0 = row0(k), r1 = row0(k + 1);
+        e = cudaMemcpyAsync(c.d_in + r0 * pitch, h_in + r0 * pitch, (size_t)(r1 - r0) * pitch,
+                            cudaMemcpyHostToDevice, c.s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(c.ev_in[k], c.s_in);
+    }
     if (e != cudaSuccess) return cuda_fail(e, "H2D");
-    rc = run(c.d_in, H, W, 0, H, 3LL * W, 0, c.d_out, 0, H, 3LL * W, 0, 1, prm, c.ws,
-             dfg_workspace_bytes((int64_t)px), stream, nullptr);
-    if (rc) return rc;
-    e = cudaMemcpyAsync(h_out, c.d_out, 3 * px, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H");
-    e = cudaStreamSynchronize(st);
+    for (int k = 0; k < nb; k++) {
+        const int r0 = row0(k), r1 = row0(k + 1);
+        int need = 0;  // last band whose rows the windows of band k reach
+        while (need + 1 < nb && row0(need + 1) < r1 + h) need++;
+        e = cudaStreamWaitEvent(st, c.ev_in[need], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "band dependency");
+        rc = run(c.d_in, H, W, 0, H, pitch, 0, c.d_out + r0 * pitch, r0, r1 - r0, pitch, 0, 1, prm, c.ws,
+                 dfg_workspace_bytes((int64_t)px), stream, nullptr);
+        if (rc) return rc;
+        e = cudaEventRecord(c.ev_k[k], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_out, c.ev_k[k], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h_out + r0 * pitch, c.d_out + r0 * pitch, (size_t)(r1 - r0) * pitch,
+                                cudaMemcpyDeviceToHost, c.s_out);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H");
+    }
+    e = cudaEventRecord(c.ev_done, c.s_out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_done, 0);  // later work on `stream` sees the result
+    if (e == cudaSuccess) e = cudaEventSynchronize(c.ev_done);
     if (e != cudaSuccess) return cuda_fail(e, "synchronize");
     return DFG_OK;
 }

@@ -33,6 +33,8 @@
 // acosf(dot * rsqrt * rsqrt) loses ~1% of decisions.
 #pragma once
 
+#include <stdlib.h>
+
 #include <type_traits>
 
 #include "dfg_f64.cuh"
@@ -796,6 +798,9 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
 // Per (window, family) launch shape: OPT outputs per thread (register
 // blocking), TR thread-rows per CTA, MINB CTAs per SM.  Register-resident
 // state per output is n (BVDF/VMF), 2n (DDF) or 4n (ACWDDF) floats.
+template <int FAM, int ST, int PC>
+cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp);  // dfg_w3.cuh
+
 template <int S, int FAM>
 struct Shape {
     static constexpr int AGG = (FAM == FAM_ACWDDF ? 4 : (FAM == FAM_DDF ? 2 : 1)) * S * S;
@@ -815,6 +820,12 @@ struct Shape {
 template <int S, int FAM, int ST, int PC>
 cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp)
 {
+    if constexpr (S == 3) {
+        // 3x3: the warp-synchronous row-sweep kernel (dfg_w3.cuh); the CTA
+        // kernel stays selectable for comparison (DFG_S3_CTA=1)
+        static const bool use_cta = getenv("DFG_S3_CTA") != nullptr;
+        if (!use_cta) return launch_w3<FAM, ST, PC>(st, in, out, kp);
+    }
     using SH = Shape<S, FAM>;
     using C = Cfg<S, FAM, SH::OPT, SH::TR>;
     auto kern = dfg_fast_kernel<S, FAM, ST, PC, SH::OPT, SH::TR, SH::MINB>;

@@ -1,0 +1,347 @@
+// dfg_w3.cuh -- warp-synchronous 3x3 kernel (BVDF / DDF / ACWDDF / VMF).
+//
+// Same arithmetic, error budget and float64 re-decision as dfg_fast.cuh, with
+// a schedule built for the small window: every warp owns a strip of 32 input
+// columns (28 output columns, lanes 2..29) and sweeps DOWN a chunk of rows.
+// Per row step each lane
+//   1. stages its new pixel into a warp-private 3-row ring of records,
+//   2. evaluates the 12 pairs whose LOWER pixel is that pixel
+//      (E_d(q) = d(q - d, q) for the 12 canonical offsets d: 2 in its row,
+//      5 in each of the two rows above) -- each unique pixel pair once --
+//      with the packed f32x2 pair math, into a 3-row ring of pair values,
+//   3. aggregates the 36 window pairs of the output pixel one row above
+//      (its own and its two neighbours' ring entries) and selects.
+// Only __syncwarp orders the ring; no CTA barrier, no halo-row recomputation
+// (the reference's row loop, _engine.py:232-487, streams rows the same way).
+#pragma once
+
+#include "dfg_fast.cuh"
+
+namespace dfg {
+
+template <int FAM>
+struct W3Cfg {
+    static constexpr bool NEED_A = FAM != FAM_VMF;
+    static constexpr bool NEED_L = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
+    static constexpr bool BOTH = NEED_A && NEED_L;
+    using DT = typename std::conditional<BOTH, float2, float>::type;
+    static constexpr int WARPS = 4;
+    static constexpr int LANES_E = 34;  // ring row width in elements (pads for pair loads at lane 31)
+    // per-warp shared layout (bytes)
+    static constexpr int REC_BYTES = 3 * LANES_E * 32;         // 2 x float4 per element (A, B)
+    static constexpr int COL_BYTES = 3 * 32 * 4;               // packed colours
+    static constexpr int E_BYTES = 3 * 12 * 32 * (int)sizeof(DT);
+    static constexpr int F64_BYTES = 9 * (int)sizeof(E64) + 2 * 36 * 8 + 16;
+    static constexpr int WARP_BYTES = (REC_BYTES + COL_BYTES + E_BYTES + F64_BYTES + 15) & ~15;
+    static constexpr size_t kSmem = (size_t)WARPS * WARP_BYTES;
+};
+
+// canonical offset index k of (du, dv): du = 0 -> dv 1, 2 (k 0, 1);
+// du = 1 -> dv -2..2 (k 2..6); du = 2 -> dv -2..2 (k 7..11)
+__host__ __device__ constexpr int w3_k(int du, int dv) { return du == 0 ? dv - 1 : 2 + (du - 1) * 5 + (dv + 2); }
+
+template <int FAM, int ST, int PC>
+__global__ void __launch_bounds__(128, 4)
+dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const KParams kp, int rows_per_chunk,
+              int n_strips, int n_chunks)
+{
+    using C = W3Cfg<FAM>;
+    using DT = typename C::DT;
+    constexpr bool ACW = FAM == FAM_ACWDDF;
+    constexpr bool BOTH = C::BOTH;
+    constexpr int N = 9, DC = 4;
+
+    extern __shared__ __align__(16) unsigned char w3_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = blockIdx.x * C::WARPS + warp;  // global warp id within the frame
+    if (gw >= n_strips * n_chunks) return;        // whole warp exits together
+    const int strip = gw % n_strips, chunk = gw / n_strips;
+    const int frame = blockIdx.z;
+    const uint8_t *fin = in + (long long)frame * kp.in_fstride;
+
+    unsigned char *wb = w3_smem + warp * C::WARP_BYTES;
+    float4 *rA = reinterpret_cast<float4 *>(wb);                 // [3][LANES_E]
+    float4 *rB = rA + 3 * C::LANES_E;
+    uint32_t *rK = reinterpret_cast<uint32_t *>(wb + C::REC_BYTES);  // [3][32]
+    DT *rE = reinterpret_cast<DT *>(wb + C::REC_BYTES + C::COL_BYTES);  // [3][12][32]
+    unsigned char *f64b = wb + C::REC_BYTES + C::COL_BYTES + C::E_BYTES;
+
+    const int col = strip * 28 - 2 + lane;  // input column of this lane
+    const int colr = resolve_idx(col, kp.W, kp.border);
+    const int oy0 = chunk * rows_per_chunk;  // first output row (strip-local) of the chunk
+    const int oy1 = min(kp.out_rows, oy0 + rows_per_chunk);
+    const float er = kp.er, ea = kp.ea;
+
+    // pad elements (lanes 32, 33) of every ring row: neutral, never used
+    if (lane < 2) {
+        for (int r = 0; r < 3; r++) {
+            rA[r * C::LANES_E + 32 + lane] = make_float4(1.f, 1.f, 1.f, 1.f);
+            rB[r * C::LANES_E + 32 + lane] = make_float4(1.f, 1.f, 1.f, 1.f);
+        }
+    }
+
+    bool zr0 = false, zr1 = false;  // zero vectors in the two previous staged rows
+    // row step y (strip-local input row, window of output row y - 1)
+    for (int y = oy0 - 1; y <= oy1; y++) {
+        const int slot = (y + 3) % 3;
+        __syncwarp();  // the previous step's readers are done with this slot
+        // ---- 1. stage the new pixel ---------------------------------------
+        int gy = resolve_idx(kp.out_row0 + y, kp.global_H, kp.border) - kp.in_row0;
+        gy = min(max(gy, 0), kp.in_rows - 1);
+        const uint8_t *px = fin + (long long)gy * kp.in_pitch + colr * 3;
+        const uint32_t r8 = px[0], g8 = px[1], b8 = px[2];
+        const bool zero = (r8 | g8 | b8) == 0;
+        Pix q;
+        q.x = zero ? 1.f : (float)r8;
+        q.y = zero ? 1.f : (float)g8;
+        q.z = zero ? 1.f : (float)b8;
+        float aux = 0.f;
+        if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(q.z, q.z, fmaf(q.y, q.y, q.x * q.x)));
+        if (ST == ST_CHROMA) aux = __frcp_rn(q.x + q.y + q.z);
+        q.aux = __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
+        {
+            float *ea4 = reinterpret_cast<float *>(rA + slot * C::LANES_E + lane);
+            float *eb4 = reinterpret_cast<float *>(rB + slot * C::LANES_E + lane);
+            ea4[0] = q.x; ea4[2] = q.y; eb4[0] = q.z; eb4[2] = q.aux;
+            if (lane > 0) {
+                ea4[-4 + 1] = q.x; ea4[-4 + 3] = q.y; eb4[-4 + 1] = q.z; eb4[-4 + 3] = q.aux;
+            }
+            rK[slot * 32 + lane] = r8 | (g8 << 8) | (b8 << 16);
+        }
+        const bool zr2 = __any_sync(0xffffffffu, zero);
+        const bool zchk = C::NEED_L && (zr0 || zr1 || zr2);  // pairs reach two rows up
+        zr0 = zr1;
+        zr1 = zr2;
+        __syncwarp();
+        // ---- 2. pair values with lower pixel q ------------------------------
+        // partner pairs (p, p+1) as packed elements: row y: lanes (l-2, l-1);
+        // rows y-1, y-2: lanes (l-2,l-1), (l,l+1), (l+2, l+3: dummy)
+        auto eval = [&](auto zc_c) {
+            constexpr bool ZC = decltype(zc_c)::value;
+            auto step = [&](int rslot, int el, P2 &da, P2 &dl) {
+                const ulonglong2 A2 = reinterpret_cast<const ulonglong2 *>(rA + rslot * C::LANES_E)[el];
+                const ulonglong2 B2 = reinterpret_cast<const ulonglong2 *>(rB + rslot * C::LANES_E)[el];
+                const Pair2 p = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
+                pair_values2<FAM, ST, PC, ZC>(q, p, kp, da, dl);
+            };
+            auto put = [&](int k, float a, float l) {
+                DT v;
+                if constexpr (BOTH) v = make_float2(a, l);
+                else if constexpr (C::NEED_A) v = a;
+                else v = l;
+                rE[(slot * 12 + k) * 32 + lane] = v;
+            };
+            const int el_m2 = max(lane - 2, 0);  // lanes 0, 1: partners outside the strip (values unused)
+            P2 da, dl;
+            // du = 0: partners (l-2, l-1) = dv 2, 1
+            step(slot, el_m2, da, dl);
+            put(w3_k(0, 2), lo2(da), lo2(dl));
+            put(w3_k(0, 1), hi2(da), hi2(dl));
+#pragma unroll
+            for (int du = 1; du <= 2; du++) {
+                const int rs = (y - du + 3) % 3;
+                step(rs, el_m2, da, dl);  // partners l-2, l-1 -> dv = 2, 1
+                put(w3_k(du, 2), lo2(da), lo2(dl));
+                put(w3_k(du, 1), hi2(da), hi2(dl));
+                step(rs, lane, da, dl);  // partners l, l+1 -> dv = 0, -1
+                put(w3_k(du, 0), lo2(da), lo2(dl));
+                put(w3_k(du, -1), hi2(da), hi2(dl));
+                step(rs, lane + 2, da, dl);  // partner l+2 -> dv = -2 (l+3 dummy)
+                put(w3_k(du, -2), lo2(da), lo2(dl));
+            }
+        };
+        if (zchk) eval(std::true_type{});
+        else eval(std::false_type{});
+        __syncwarp();
+        // ---- 3. aggregate + select for output row y - 1 ---------------------
+        const int oy = y - 1;
+        if (oy < oy0) continue;  // warm-up rows (uniform across the warp)
+        const bool valid = lane >= 2 && lane < 30 && oy < oy1 && col < kp.W;
+        P2 ag[BOTH ? N : 1], cen[ACW ? N : 1];
+        float aS[BOTH ? 1 : N];
+#pragma unroll
+        for (int i = 0; i < N; i++) {
+            if constexpr (BOTH) ag[i] = pk2(kp.self_term, 0.f);
+            else aS[i] = C::NEED_A ? kp.self_term : 0.f;
+        }
+        if constexpr (ACW) cen[DC] = pk2(kp.self_term, 0.f);
+        const int lc = min(max(lane, 1), 30);  // clamp so lanes 0/31 read in-bounds (results unused)
+#pragma unroll
+        for (int j = 1; j < N; j++) {
+#pragma unroll
+            for (int i = 0; i < j; i++) {
+                const int du = j / 3 - i / 3, dv = j % 3 - i % 3;
+                const int k = w3_k(du, dv);
+                // lower pixel j: window row j/3 -> input row oy - 1 + j/3, lane lc - 1 + j%3
+                const int rs = (oy - 1 + j / 3 + 3) % 3;
+                const DT val = rE[(rs * 12 + k) * 32 + lc - 1 + j % 3];
+                if constexpr (BOTH) {
+                    const P2 x = *reinterpret_cast<const P2 *>(&val);
+                    ag[i] = add2(ag[i], x);
+                    ag[j] = add2(ag[j], x);
+                    if constexpr (ACW) {
+                        if (j == DC) cen[i] = x;
+                        else if (i == DC) cen[j] = x;
+                    }
+                } else {
+                    aS[i] += val;
+                    aS[j] += val;
+                }
+            }
+        }
+        // colours of the window (rings hold input rows oy-1, oy, oy+1)
+        uint32_t wc[N];
+#pragma unroll
+        for (int i = 0; i < N; i++) wc[i] = rK[((oy - 1 + i / 3 + 3) % 3) * 32 + lc - 1 + i % 3];
+        int b;
+        bool doubt;
+        if constexpr (ACW) {
+            Sel sd, s0, s1, s2;
+            const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                const float a = lo2(ag[i]), l = hi2(ag[i]);
+                const float ad = lo2(cen[i]), ld = hi2(cen[i]);
+                const float pd = a * l;
+                const float l0 = fmaf(w0, ld, l), l1 = fmaf(w1, ld, l), l2 = fmaf(w2, ld, l);
+                const float p0 = fmaf(w0, ad, a) * l0, p1 = fmaf(w1, ad, a) * l1, p2 = fmaf(w2, ad, a) * l2;
+                if (i == 0) {
+                    sd.init(pd, l, wc[i], 0.f, 0.f);
+                    s0.init(p0, l0, wc[i], ad, ld);
+                    s1.init(p1, l1, wc[i], ad, ld);
+                    s2.init(p2, l2, wc[i], ad, ld);
+                } else {
+                    sd.add(pd, l, i, wc[i], 0.f, 0.f);
+                    s0.add(p0, l0, i, wc[i], ad, ld);
+                    s1.add(p1, l1, i, wc[i], ad, ld);
+                    s2.add(p2, l2, i, wc[i], ad, ld);
+                }
+            }
+            float a = s0.xa;
+            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
+            float sv = a * s0.xl;
+            a = s1.xa;
+            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
+            sv = fmaf(a, s1.xl, sv);
+            a = s2.xa;
+            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
+            sv = fmaf(a, s2.xl, sv);
+            const float ld_sum = s0.xl + s1.xl + s2.xl;
+            const float es = 4.f * er * fmaxf(fabsf(sv), kp.threshold) +
+                             2.f * kp.ea_pair * (ST == ST_CHROMA ? kp.slope : 1.f) * ld_sum + 1e-6f;
+            const bool fires = sv > kp.threshold;
+            b = fires ? sd.i1 : DC;
+            const float er2 = 2.f * er, ea2 = 2.f * ea;
+            doubt = s0.doubtful(er2, ea2) || s1.doubtful(er2, ea2) || s2.doubtful(er2, ea2) ||
+                    fabsf(sv - kp.threshold) <= es || (fires && sd.doubtful(er2, ea2));
+        } else {
+            Sel sl;
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                float v, l;
+                if constexpr (FAM == FAM_BVDF) {
+                    v = aS[i];
+                    l = 1.f;
+                } else if constexpr (FAM == FAM_VMF) {
+                    v = aS[i];
+                    l = 0.f;
+                } else {
+                    l = hi2(ag[i]);
+                    v = lo2(ag[i]) * l;
+                }
+                if (i == 0) sl.init(v, l, wc[i], 0.f, 0.f);
+                else sl.add(v, l, i, wc[i], 0.f, 0.f);
+            }
+            b = sl.i1;
+            doubt = (FAM == FAM_DDF) ? sl.doubtful(2.f * er, 2.f * ea) : sl.doubtful(er, ea);
+        }
+        uint8_t *orow = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch;
+        if (kp.dbg != nullptr && valid) {
+            float *d = kp.dbg + ((long long)frame * kp.out_rows * kp.W + (long long)oy * kp.W + col) * (2 * N);
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                if constexpr (BOTH) {
+                    d[i] = lo2(ag[i]);
+                    d[N + i] = hi2(ag[i]);
+                } else {
+                    d[i] = C::NEED_A ? aS[i] : 0.f;
+                    d[N + i] = C::NEED_L ? aS[i] : 0.f;
+                }
+            }
+        }
+        if (valid) {
+            uint32_t cb = wc[0];
+#pragma unroll
+            for (int i = 1; i < N; i++) cb = (b == i) ? wc[i] : cb;
+            uint8_t *op = orow + col * 3;
+            op[0] = (uint8_t)(cb & 0xff);
+            op[1] = (uint8_t)((cb >> 8) & 0xff);
+            op[2] = (uint8_t)((cb >> 16) & 0xff);
+        }
+        // ---- 4. float64 re-decision of doubtful pixels (whole warp) -------
+        unsigned mask = __ballot_sync(0xffffffffu, valid && doubt);
+        if (mask) {
+            if (lane == 0) atomicAdd(kp.flag_count, (unsigned)__popc(mask));
+            E64 *e64 = reinterpret_cast<E64 *>(f64b);
+            double *dA = reinterpret_cast<double *>(e64 + N);
+            double *dL = dA + 36;
+            while (mask) {
+                const int fl = __ffs(mask) - 1;
+                mask &= mask - 1;
+                if (lane < N) {
+                    const int i = lane;
+                    const uint32_t cc = rK[((oy - 1 + i / 3 + 3) % 3) * 32 + fl - 1 + i % 3];
+                    prep64(make_float4((float)(cc & 0xff), (float)((cc >> 8) & 0xff), (float)((cc >> 16) & 0xff), 0.f),
+                           ST, e64[i]);
+                }
+                __syncwarp();
+                pair_tables<false>(e64, kp.fp, lane, 32, dA, dL, C::NEED_A, C::NEED_L);
+                __syncwarp();
+                double m;
+                int bb = decide64(e64, kp.fp, lane, dA, dL, &m);
+                if (ST == ST_EXACT && C::NEED_A && m < kp.fp.cr_margin) {
+                    if (lane == 0) atomicAdd(kp.flag_count + 1, 1u);
+                    __syncwarp();
+                    pair_tables<true>(e64, kp.fp, lane, 32, dA, dL, C::NEED_A, C::NEED_L);
+                    __syncwarp();
+                    bb = decide64(e64, kp.fp, lane, dA, dL, &m);
+                }
+                if (lane == 0) {
+                    uint8_t *op = orow + (strip * 28 - 2 + fl) * 3;
+                    op[0] = (uint8_t)e64[bb].raw[0];
+                    op[1] = (uint8_t)e64[bb].raw[1];
+                    op[2] = (uint8_t)e64[bb].raw[2];
+                }
+                __syncwarp();
+            }
+        }
+    }
+}
+
+template <int FAM, int ST, int PC>
+cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp)
+{
+    using C = W3Cfg<FAM>;
+    auto kern = dfg_w3_kernel<FAM, ST, PC>;
+    static unsigned long long configured = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(configured & (1ull << (dev & 63)))) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
+        if (e != cudaSuccess) return e;
+        configured |= 1ull << (dev & 63);
+    }
+    const int n_strips = (kp.W + 27) / 28;
+    // rows per chunk: about one wave of resident warps (16 per SM), more
+    // rows (fewer warm-up rows, 2 per chunk) when the input is taller
+    const long long strip_rows = (long long)n_strips * kp.out_rows * kp.n_frames;
+    int rpc = (int)(strip_rows / (148 * 16));
+    rpc = rpc < 16 ? 16 : (rpc > 64 ? 64 : rpc);
+    const int n_chunks = (kp.out_rows + rpc - 1) / rpc;
+    const int warps = n_strips * n_chunks;
+    dim3 grid((warps + C::WARPS - 1) / C::WARPS, 1, kp.n_frames);
+    kern<<<grid, C::WARPS * 32, C::kSmem, st>>>(in, out, kp, rpc, n_strips, n_chunks);
+    return cudaGetLastError();
+}
+
+}  // namespace dfg

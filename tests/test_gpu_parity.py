@@ -163,3 +163,18 @@ def test_invalid_inputs_raise(cuda):
         apply_filter(RasterImage(np.full((4, 4, 3), 256.0)), parse_filter_spec("vmf"))
     with pytest.raises(NotImplementedError):
         apply_filter(RasterImage(np.full((4, 4, 3), 5.0)), parse_filter_spec("vmf:window=9"))
+
+
+@pytest.mark.parametrize("spec,border", [("ddf:exact:window=7", "reflect"), ("acwddf:minimax:window=5", "replicate"),
+                                         ("bvdf:rgb", "reflect")])
+def test_host_pipeline_bands(cuda, spec, border):
+    """dfg_filter_host pipelines H2D / kernel / D2H over row bands; bands
+    must reproduce the whole-image device call exactly."""
+    torch = cuda
+    img = synth.noisy_image(1100, 190, 5, ("correlated", 0.2))
+    s = parse_filter_spec(spec)
+    pin = torch.from_numpy(img).pin_memory()
+    out = torch.empty_like(pin).pin_memory()
+    a = filter_host(pin.numpy(), s, _policy(border), out=out.numpy())
+    b = filter_device(torch.from_numpy(img).cuda(), s, _policy(border)).cpu().numpy()
+    assert (a == b).all()
