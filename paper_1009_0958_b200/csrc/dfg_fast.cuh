@@ -823,8 +823,13 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
     if constexpr (S == 3) {
         // 3x3: the warp-synchronous row-sweep kernel (dfg_w3.cuh); the CTA
         // kernel stays selectable for comparison (DFG_S3_CTA=1)
-        static const bool use_cta = getenv("DFG_S3_CTA") != nullptr;
-        if (!use_cta) return launch_w3<FAM, ST, PC>(st, in, out, kp);
+        // for small inputs (too few strip-rows to fill the SMs with sweeping
+        // warps) the CTA kernel's finer tiles win
+        // (DFG_S3_KERNEL=cta|w3 forces one; read per call so tests can switch)
+        const char *force = getenv("DFG_S3_KERNEL");
+        const long long strip_rows = (long long)((kp.W + 27) / 28) * kp.out_rows * kp.n_frames;
+        const bool w3 = force ? (force[0] == 'w') : (strip_rows >= 32768);
+        if (w3) return launch_w3<FAM, ST, PC>(st, in, out, kp);
     }
     using SH = Shape<S, FAM>;
     using C = Cfg<S, FAM, SH::OPT, SH::TR>;
