@@ -81,15 +81,25 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
     }
 
     bool zr0 = false, zr1 = false;  // zero vectors in the two previous staged rows
+    // the pixel of the next row step is loaded one step ahead (its HBM
+    // latency hides behind the current step's pair math)
+    auto load_px = [&](int yy, uint32_t &r, uint32_t &g, uint32_t &b) {
+        int gy = resolve_idx(kp.out_row0 + yy, kp.global_H, kp.border) - kp.in_row0;
+        gy = min(max(gy, 0), kp.in_rows - 1);
+        const uint8_t *px = fin + (long long)gy * kp.in_pitch + colr * 3;
+        r = px[0];
+        g = px[1];
+        b = px[2];
+    };
+    uint32_t nr8, ng8, nb8;
+    load_px(oy0 - 1, nr8, ng8, nb8);
     // row step y (strip-local input row, window of output row y - 1)
     for (int y = oy0 - 1; y <= oy1; y++) {
         const int slot = (y + 3) % 3;
         __syncwarp();  // the previous step's readers are done with this slot
         // ---- 1. stage the new pixel ---------------------------------------
-        int gy = resolve_idx(kp.out_row0 + y, kp.global_H, kp.border) - kp.in_row0;
-        gy = min(max(gy, 0), kp.in_rows - 1);
-        const uint8_t *px = fin + (long long)gy * kp.in_pitch + colr * 3;
-        const uint32_t r8 = px[0], g8 = px[1], b8 = px[2];
+        const uint32_t r8 = nr8, g8 = ng8, b8 = nb8;
+        if (y < oy1) load_px(y + 1, nr8, ng8, nb8);
         const bool zero = (r8 | g8 | b8) == 0;
         Pix q;
         q.x = zero ? 1.f : (float)r8;
@@ -118,12 +128,6 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         // rows y-1, y-2: lanes (l-2,l-1), (l,l+1), (l+2, l+3: dummy)
         auto eval = [&](auto zc_c) {
             constexpr bool ZC = decltype(zc_c)::value;
-            auto step = [&](int rslot, int el, P2 &da, P2 &dl) {
-                const ulonglong2 A2 = reinterpret_cast<const ulonglong2 *>(rA + rslot * C::LANES_E)[el];
-                const ulonglong2 B2 = reinterpret_cast<const ulonglong2 *>(rB + rslot * C::LANES_E)[el];
-                const Pair2 p = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
-                pair_values2<FAM, ST, PC, ZC>(q, p, kp, da, dl);
-            };
             auto put = [&](int k, float a, float l) {
                 DT v;
                 if constexpr (BOTH) v = make_float2(a, l);
@@ -132,22 +136,32 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                 rE[(slot * 12 + k) * 32 + lane] = v;
             };
             const int el_m2 = max(lane - 2, 0);  // lanes 0, 1: partners outside the strip (values unused)
-            P2 da, dl;
+            // all partner loads first, then the seven independent packed pair
+            // evaluations, then the stores: the pair math chains interleave
+            const int rs1 = (y + 2) % 3, rs2 = (y + 1) % 3;
+            const int rsl[7] = {slot, rs1, rs1, rs1, rs2, rs2, rs2};
+            const int els[7] = {el_m2, el_m2, lane, lane + 2, el_m2, lane, lane + 2};
+            Pair2 pp[7];
+#pragma unroll
+            for (int t = 0; t < 7; t++) {
+                const ulonglong2 A2 = reinterpret_cast<const ulonglong2 *>(rA + rsl[t] * C::LANES_E)[els[t]];
+                const ulonglong2 B2 = reinterpret_cast<const ulonglong2 *>(rB + rsl[t] * C::LANES_E)[els[t]];
+                pp[t] = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
+            }
+            P2 da[7], dl[7];
+#pragma unroll
+            for (int t = 0; t < 7; t++) pair_values2<FAM, ST, PC, ZC>(q, pp[t], kp, da[t], dl[t]);
             // du = 0: partners (l-2, l-1) = dv 2, 1
-            step(slot, el_m2, da, dl);
-            put(w3_k(0, 2), lo2(da), lo2(dl));
-            put(w3_k(0, 1), hi2(da), hi2(dl));
+            put(w3_k(0, 2), lo2(da[0]), lo2(dl[0]));
+            put(w3_k(0, 1), hi2(da[0]), hi2(dl[0]));
 #pragma unroll
             for (int du = 1; du <= 2; du++) {
-                const int rs = (y - du + 3) % 3;
-                step(rs, el_m2, da, dl);  // partners l-2, l-1 -> dv = 2, 1
-                put(w3_k(du, 2), lo2(da), lo2(dl));
-                put(w3_k(du, 1), hi2(da), hi2(dl));
-                step(rs, lane, da, dl);  // partners l, l+1 -> dv = 0, -1
-                put(w3_k(du, 0), lo2(da), lo2(dl));
-                put(w3_k(du, -1), hi2(da), hi2(dl));
-                step(rs, lane + 2, da, dl);  // partner l+2 -> dv = -2 (l+3 dummy)
-                put(w3_k(du, -2), lo2(da), lo2(dl));
+                const int t = 1 + 3 * (du - 1);
+                put(w3_k(du, 2), lo2(da[t]), lo2(dl[t]));  // partners l-2, l-1 -> dv = 2, 1
+                put(w3_k(du, 1), hi2(da[t]), hi2(dl[t]));
+                put(w3_k(du, 0), lo2(da[t + 1]), lo2(dl[t + 1]));  // partners l, l+1 -> dv = 0, -1
+                put(w3_k(du, -1), hi2(da[t + 1]), hi2(dl[t + 1]));
+                put(w3_k(du, -2), lo2(da[t + 2]), lo2(dl[t + 2]));  // partner l+2 -> dv = -2
             }
         };
         if (zchk) eval(std::true_type{});
@@ -166,6 +180,10 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         }
         if constexpr (ACW) cen[DC] = pk2(kp.self_term, 0.f);
         const int lc = min(max(lane, 1), 30);  // clamp so lanes 0/31 read in-bounds (results unused)
+        // ring rows of the window's input rows oy-1, oy, oy+1 (slots of y-2, y-1, y)
+        const int s0 = (oy + 2) % 3, s1 = (oy + 3) % 3, s2 = slot;
+        const DT *eR[3] = {rE + s0 * 12 * 32 + lc - 1, rE + s1 * 12 * 32 + lc - 1, rE + s2 * 12 * 32 + lc - 1};
+        const uint32_t *kR[3] = {rK + s0 * 32 + lc - 1, rK + s1 * 32 + lc - 1, rK + s2 * 32 + lc - 1};
 #pragma unroll
         for (int j = 1; j < N; j++) {
 #pragma unroll
@@ -173,8 +191,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                 const int du = j / 3 - i / 3, dv = j % 3 - i % 3;
                 const int k = w3_k(du, dv);
                 // lower pixel j: window row j/3 -> input row oy - 1 + j/3, lane lc - 1 + j%3
-                const int rs = (oy - 1 + j / 3 + 3) % 3;
-                const DT val = rE[(rs * 12 + k) * 32 + lc - 1 + j % 3];
+                const DT val = eR[j / 3][k * 32 + j % 3];
                 if constexpr (BOTH) {
                     const P2 x = *reinterpret_cast<const P2 *>(&val);
                     ag[i] = add2(ag[i], x);
@@ -192,7 +209,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         // colours of the window (rings hold input rows oy-1, oy, oy+1)
         uint32_t wc[N];
 #pragma unroll
-        for (int i = 0; i < N; i++) wc[i] = rK[((oy - 1 + i / 3 + 3) % 3) * 32 + lc - 1 + i % 3];
+        for (int i = 0; i < N; i++) wc[i] = kR[i / 3][i % 3];
         int b;
         bool doubt;
         if constexpr (ACW) {
