@@ -382,7 +382,11 @@ struct Cfg {
         return o;
     }
     static constexpr int NPL = (G == S) ? plane_off(S - 1) + ndv_of(S - 1) : NDV;  // planes resident at once
-    static constexpr size_t kSmem = (size_t)RECN * 32 + (size_t)RN4 * 4 + (size_t)NPL * RN * sizeof(DT);
+    // 5x5 / 7x7: row-segment sums S_+du / S_-du (S values per pixel each)
+    static constexpr bool SEG = S >= 5;
+    static constexpr int SEGN = SEG ? 2 * S : 0;
+    static constexpr size_t kSmem =
+        (size_t)RECN * 32 + (size_t)RN4 * 4 + (size_t)NPL * RN * sizeof(DT) + (size_t)SEGN * RN * sizeof(DT);
 };
 
 // One-pass first-strict-minimum with "best competitor of a different colour"
@@ -445,6 +449,191 @@ __device__ __forceinline__ void pair_values2(const Pix &p, const Pair2 &q, const
                      minkowski<PC>(a, rawrec(hi2(q.x), hi2(q.y), hi2(q.z), hi2(q.aux)), kp));
         }
     }
+}
+
+__device__ __forceinline__ float dt_add(float a, float b) { return a + b; }
+__device__ __forceinline__ float2 dt_add(float2 a, float2 b)
+{
+    const P2 r = add2(*reinterpret_cast<const P2 *>(&a), *reinterpret_cast<const P2 *>(&b));
+    return *reinterpret_cast<const float2 *>(&r);
+}
+__device__ __forceinline__ float dt_zero(float) { return 0.f; }
+__device__ __forceinline__ float2 dt_zero(float2) { return make_float2(0.f, 0.f); }
+
+// Row-segment sums of one pixel: T[t], t = dv + S - 1, dv in [-(S-1), S-1]
+// (distances to the pixels of one row at column offsets dv) ->
+// Sg[v] = sum_{dv = -v}^{S-1-v} T = the distance sum to the S-wide segment of
+// a window in which the pixel sits at column v.  Every window contains
+// dv = 0, so Sg[v] = L[S-1-v] + R[2S-2-v] with suffix sums L of the left part
+// and prefix sums R of the right part: additions only (no cancellation),
+// 3S-4 adds for all S windows.
+template <int S, typename DT>
+__device__ __forceinline__ void seg_sums(const DT (&T)[2 * S - 1], DT (&Sg)[S])
+{
+    DT L[S - 1], R[S];
+    L[S - 2] = T[S - 2];
+#pragma unroll
+    for (int t = S - 3; t >= 0; t--) L[t] = dt_add(T[t], L[t + 1]);
+    R[0] = T[S - 1];
+#pragma unroll
+    for (int t = 1; t < S; t++) R[t] = dt_add(R[t - 1], T[S - 1 + t]);
+    Sg[0] = R[S - 1];
+#pragma unroll
+    for (int v = 1; v < S; v++) Sg[v] = dt_add(L[S - 1 - v], R[S - 1 - v]);
+}
+
+// 5x5 / 7x7 aggregation by row segments.  For row offset du, stage 1 evaluates
+// the pair planes D_(du,dv)(p) and, from the same registers, the pixel's
+// downward segment sums S_+du(p, v); after a barrier the upward sums
+// S_-du(q, v) are read off the planes (the pairs whose upper pixel is in the
+// row above); after a second barrier each output adds, for each window
+// candidate (u, v), S_+du(q, v) if u + du < S and S_-du(q, v) if u >= du:
+// agg(u, v) = sum_dy S_dy(q, v) covers every other window pixel exactly once.
+// s^3 segment loads per output instead of n(n-1)/2 pair loads (343 vs 1176
+// for 7x7), and the sums carry no cancellation.
+template <int S, int FAM, int ST, int PC, int OPT, int TR, typename AG, typename CE, typename AA, typename AL>
+__device__ __forceinline__ void seg_stages(const float4 *sA, const float4 *sB, typename Cfg<S, FAM, OPT, TR>::DT *sD,
+                                           bool zchk, const KParams &kp, AG &ag, CE &cen, AA &aA, AL &aL)
+{
+    using C = Cfg<S, FAM, OPT, TR>;
+    using DT = typename C::DT;
+    constexpr int H = C::H, N = C::N, DC = C::DC, RW = C::RW, RH = C::RH, RN = C::RN, NT = C::NT;
+    constexpr int RWS = C::RWS, PADC = C::PADC, NDV = C::NDV;
+    constexpr bool ACW = FAM == FAM_ACWDDF;
+    constexpr bool BOTH = C::BOTH;
+    DT *sP = sD + C::NPL * RN;  // S_+du [v][RN]
+    DT *sM = sP + S * RN;       // S_-du [v][RN]
+    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+
+    static_for<0, S>([&](auto du_c) {
+        constexpr int du = decltype(du_c)::value;
+        constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
+        constexpr int ndv = C::ndv_of(du);
+        constexpr int NK2 = (ndv + 1) / 2;
+        // ---- stage 1: planes (+ downward segment sums for du > 0) ---------
+        auto stage1 = [&](auto zc_c) {
+            constexpr bool ZC = decltype(zc_c)::value;
+            constexpr int items = (RH - du) * RW;
+            for (int it = tid; it < items; it += NT) {
+                const int py = it / RW, px = it - py * RW;
+                const int pidx = py * RWS + PADC + px;
+                const float4 a4 = sA[pidx], b4 = sB[pidx];
+                const Pix p = {a4.x, a4.z, b4.x, b4.z};
+                const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
+                const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
+                DT T[NDV];
+#pragma unroll
+                for (int kk = 0; kk < NK2; kk++) {
+                    const ulonglong2 A2 = qa[2 * kk], B2 = qb[2 * kk];
+                    const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
+                    P2 da, dl;
+                    pair_values2<FAM, ST, PC, ZC>(p, q, kp, da, dl);
+                    DT v0, v1;
+                    if constexpr (BOTH) {
+                        v0 = make_float2(lo2(da), lo2(dl));
+                        v1 = make_float2(hi2(da), hi2(dl));
+                    } else if constexpr (C::NEED_A) {
+                        v0 = lo2(da);
+                        v1 = hi2(da);
+                    } else {
+                        v0 = lo2(dl);
+                        v1 = hi2(dl);
+                    }
+                    sD[(2 * kk) * RN + it] = v0;
+                    T[2 * kk] = v0;
+                    if (2 * kk + 1 < ndv) {
+                        sD[(2 * kk + 1) * RN + it] = v1;
+                        T[2 * kk + 1] = v1;
+                    }
+                }
+                if constexpr (du > 0) {  // here k = dv + S - 1 = t
+                    DT Sg[S];
+                    seg_sums<S>(T, Sg);
+#pragma unroll
+                    for (int v = 0; v < S; v++) sP[v * RN + it] = Sg[v];
+                }
+            }
+        };
+        if (zchk) stage1(std::true_type{});
+        else stage1(std::false_type{});
+        __syncthreads();
+        // ---- upward segment sums (du > 0) / both sides in the row (du = 0) --
+        {
+            constexpr int items = (RH - du) * RW;
+            for (int it = tid; it < items; it += NT) {
+                const int qi = it + du * RW;  // pixel q in rows du .. RH-1
+                DT T[NDV];
+                if constexpr (du == 0) {
+#pragma unroll
+                    for (int t = 0; t < NDV; t++) {
+                        const int dv = t - (S - 1);
+                        if (dv > 0) T[t] = sD[(dv - 1) * RN + qi];
+                        else if (dv < 0) T[t] = sD[(-dv - 1) * RN + qi + dv];
+                        else T[t] = dt_zero(DT());
+                    }
+                } else {
+                    // T_q(-du, dv) = D_(du, -dv)(q + (-du, dv)): plane 2S-2-t
+#pragma unroll
+                    for (int t = 0; t < NDV; t++) {
+                        const int dv = t - (S - 1);
+                        T[t] = sD[(NDV - 1 - t) * RN + qi - du * RW + dv];
+                    }
+                }
+                DT Sg[S];
+                seg_sums<S>(T, Sg);
+                DT *dst = (du == 0) ? sP : sM;
+#pragma unroll
+                for (int v = 0; v < S; v++) dst[v * RN + qi] = Sg[v];
+            }
+        }
+        __syncthreads();
+        // ---- per-output accumulation of the segment sums --------------------
+#pragma unroll
+        for (int o = 0; o < OPT; o++) {
+            const int ry0 = ty * OPT + o;
+#pragma unroll
+            for (int u = 0; u < S; u++) {
+#pragma unroll
+                for (int v = 0; v < S; v++) {
+                    const int i = u * S + v;
+                    const int qi = (ry0 + u) * RW + tx + v;
+                    DT add = dt_zero(DT());
+                    bool any = false;
+                    if (u + du < S) {
+                        add = sP[v * RN + qi];
+                        any = true;
+                    }
+                    if (du > 0 && u >= du) {
+                        add = any ? dt_add(add, sM[v * RN + qi]) : sM[v * RN + qi];
+                        any = true;
+                    }
+                    if (any) {
+                        if constexpr (BOTH) {
+                            ag[o][i] = add2(ag[o][i], *reinterpret_cast<const P2 *>(&add));
+                        } else if constexpr (C::NEED_A) {
+                            aA[o][i] += add;
+                        } else {
+                            aL[o][i] += add;
+                        }
+                    }
+                    if constexpr (ACW) {  // centre-column stash: the pair (i, centre) itself
+                        if (i < DC && H - u == du) {
+                            const int dv = H - v;
+                            const int k = dv - dv0;
+                            const DT x = sD[k * RN + qi];
+                            cen[o][i] = *reinterpret_cast<const P2 *>(&x);
+                        } else if (i > DC && u - H == du) {
+                            const int dv = v - H;
+                            const int k = dv - dv0;
+                            const DT x = sD[k * RN + (ry0 + H) * RW + tx + H];
+                            cen[o][i] = *reinterpret_cast<const P2 *>(&x);
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();
+    });
 }
 
 template <int S, int FAM, int ST, int PC, int OPT, int TR, int MINB>
@@ -540,6 +729,9 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         if constexpr (ACW) cen[o][DC] = pk2(kp.self_term, 0.f);
     }
 
+    if constexpr (C::SEG) {
+        seg_stages<S, FAM, ST, PC, OPT, TR>(sA, sB, sD, zchk, kp, ag, cen, aA, aL);
+    } else
     static_for<0, S / C::G>([&](auto g_c) {
         constexpr int g0 = decltype(g_c)::value * C::G;
         constexpr int total = C::item_off(g0 + C::G - 1) + (RH - (g0 + C::G - 1)) * RW;

@@ -25,12 +25,15 @@ struct W3Cfg {
     static constexpr bool NEED_L = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
     static constexpr bool BOTH = NEED_A && NEED_L;
     using DT = typename std::conditional<BOTH, float2, float>::type;
-    static constexpr int WARPS = 4;
+    static constexpr int WARPS = 2;
     static constexpr int LANES_E = 34;  // ring row width in elements (pads for pair loads at lane 31)
     // per-warp shared layout (bytes)
     static constexpr int REC_BYTES = 3 * LANES_E * 32;         // 2 x float4 per element (A, B)
     static constexpr int COL_BYTES = 3 * 32 * 4;               // packed colours
-    static constexpr int E_BYTES = 3 * 12 * 32 * (int)sizeof(DT);
+    // pair-value ring: offsets k 0..6 (du 0, 1) for three rows, k 7..11 (du 2)
+    // for the current row only -- the window of the output one row up reads
+    // du <= 1 entries of the previous row and du = 0 entries two rows up
+    static constexpr int E_BYTES = (3 * 7 + 5) * 32 * (int)sizeof(DT);
     static constexpr int F64_BYTES = 9 * (int)sizeof(E64) + 2 * 36 * 8 + 16;
     static constexpr int WARP_BYTES = (REC_BYTES + COL_BYTES + E_BYTES + F64_BYTES + 15) & ~15;
     static constexpr size_t kSmem = (size_t)WARPS * WARP_BYTES;
@@ -41,7 +44,7 @@ struct W3Cfg {
 __host__ __device__ constexpr int w3_k(int du, int dv) { return du == 0 ? dv - 1 : 2 + (du - 1) * 5 + (dv + 2); }
 
 template <int FAM, int ST, int PC>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(64, 9)
 dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const KParams kp, int rows_per_chunk,
               int n_strips, int n_chunks)
 {
@@ -63,7 +66,8 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
     float4 *rA = reinterpret_cast<float4 *>(wb);                 // [3][LANES_E]
     float4 *rB = rA + 3 * C::LANES_E;
     uint32_t *rK = reinterpret_cast<uint32_t *>(wb + C::REC_BYTES);  // [3][32]
-    DT *rE = reinterpret_cast<DT *>(wb + C::REC_BYTES + C::COL_BYTES);  // [3][12][32]
+    DT *rE = reinterpret_cast<DT *>(wb + C::REC_BYTES + C::COL_BYTES);  // [3][7][32] + [5][32]
+    DT *rE2 = rE + 3 * 7 * 32;
     unsigned char *f64b = wb + C::REC_BYTES + C::COL_BYTES + C::E_BYTES;
 
     const int col = strip * 28 - 2 + lane;  // input column of this lane
@@ -133,7 +137,8 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                 if constexpr (BOTH) v = make_float2(a, l);
                 else if constexpr (C::NEED_A) v = a;
                 else v = l;
-                rE[(slot * 12 + k) * 32 + lane] = v;
+                if (k < 7) rE[(slot * 7 + k) * 32 + lane] = v;
+                else rE2[(k - 7) * 32 + lane] = v;
             };
             const int el_m2 = max(lane - 2, 0);  // lanes 0, 1: partners outside the strip (values unused)
             // all partner loads first, then the seven independent packed pair
@@ -182,7 +187,8 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         const int lc = min(max(lane, 1), 30);  // clamp so lanes 0/31 read in-bounds (results unused)
         // ring rows of the window's input rows oy-1, oy, oy+1 (slots of y-2, y-1, y)
         const int s0 = (oy + 2) % 3, s1 = (oy + 3) % 3, s2 = slot;
-        const DT *eR[3] = {rE + s0 * 12 * 32 + lc - 1, rE + s1 * 12 * 32 + lc - 1, rE + s2 * 12 * 32 + lc - 1};
+        const DT *eR[3] = {rE + s0 * 7 * 32 + lc - 1, rE + s1 * 7 * 32 + lc - 1, rE + s2 * 7 * 32 + lc - 1};
+        const DT *eR2 = rE2 + lc - 1;
         const uint32_t *kR[3] = {rK + s0 * 32 + lc - 1, rK + s1 * 32 + lc - 1, rK + s2 * 32 + lc - 1};
 #pragma unroll
         for (int j = 1; j < N; j++) {
@@ -191,7 +197,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                 const int du = j / 3 - i / 3, dv = j % 3 - i % 3;
                 const int k = w3_k(du, dv);
                 // lower pixel j: window row j/3 -> input row oy - 1 + j/3, lane lc - 1 + j%3
-                const DT val = eR[j / 3][k * 32 + j % 3];
+                const DT val = (k < 7) ? eR[j / 3][k * 32 + j % 3] : eR2[(k - 7) * 32 + j % 3];
                 if constexpr (BOTH) {
                     const P2 x = *reinterpret_cast<const P2 *>(&val);
                     ag[i] = add2(ag[i], x);
