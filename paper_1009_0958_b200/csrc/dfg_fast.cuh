@@ -362,7 +362,9 @@ struct Cfg {
     static constexpr int RH = TH + 2 * H, RW = TW + 2 * H, RN = RH * RW;
     static constexpr int RN4 = (RN + 3) & ~3;
     static constexpr int NDV = 2 * S - 1;
-    static constexpr int PADC = S, RWS = RW + 2 * S + 1;  // padded record rows (unclamped dv reads)
+    // padded record rows (unclamped dv reads); the pad is a multiple of 8
+    // elements (128 B) so a warp straddling a row wrap keeps its bank mapping
+    static constexpr int PADC = S, RWS = RW + ((2 * S + 1 + 7) & ~7);
     static constexpr int RECN = RH * RWS;
     using DT = typename std::conditional<BOTH, float2, float>::type;
     // Row offsets du are processed in groups of G (one barrier pair per
