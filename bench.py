@@ -225,10 +225,16 @@ def run_ours(args, config):
     from paper_1009_0958_b200 import filters as F
 
     world, rank, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    local = local % max(1, torch.cuda.device_count())  # (ranks sharing a GPU: gloo smoke runs only)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    backend = args.dist_backend
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    cdev = dev if backend == "nccl" else torch.device("cpu")  # where the timing reductions live
     cfg = synth.CONFIGS[config]
     spec = parse_filter_spec(cfg["spec"])
     wl = workload(config, rank, world)
@@ -277,7 +283,7 @@ def run_ours(args, config):
         dist.barrier()
     torch.cuda.synchronize()
     ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    tot = torch.tensor([sum(ms)], dtype=torch.float64, device=dev)
+    tot = torch.tensor([sum(ms)], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     tot_ms = float(tot.item())
@@ -299,7 +305,7 @@ def run_ours(args, config):
         for _ in range(args.steps):
             F.filter_host(a_in, spec, out=a_out)
         e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
-        et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+        et = torch.tensor([e_ms], dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e_ms = float(et.item())
@@ -356,6 +362,8 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
+                    help="process-group backend for the timing barrier/max (gloo only for smoke runs)")
     ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
