@@ -240,6 +240,24 @@ __device__ __forceinline__ P2 fma2(P2 a, P2 b, P2 c)
     return r;
 }
 
+// Whole 16-byte shared-memory loads.  The compiler would otherwise split a
+// record load into the two scalars it uses -- 4-byte accesses at a 16-byte
+// lane stride, a 4-way bank conflict.
+__device__ __forceinline__ float4 lds_f4(const float4 *p)
+{
+    float4 v;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ ulonglong2 lds_u2(const void *p)
+{
+    ulonglong2 v;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(p);
+    asm("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
+    return v;
+}
+
 // Scalar pixel p (gray-mapped g, aux) against a packed pixel pair Q = (q, q+1).
 struct Pix {
     float x, y, z, aux;
@@ -519,14 +537,14 @@ __device__ __forceinline__ void seg_stages(const float4 *sA, const float4 *sB, t
             for (int it = tid; it < items; it += NT) {
                 const int py = it / RW, px = it - py * RW;
                 const int pidx = py * RWS + PADC + px;
-                const float4 a4 = sA[pidx], b4 = sB[pidx];
+                const float4 a4 = lds_f4(sA + pidx), b4 = lds_f4(sB + pidx);
                 const Pix p = {a4.x, a4.z, b4.x, b4.z};
                 const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
                 const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
                 DT T[NDV];
 #pragma unroll
                 for (int kk = 0; kk < NK2; kk++) {
-                    const ulonglong2 A2 = qa[2 * kk], B2 = qb[2 * kk];
+                    const ulonglong2 A2 = lds_u2(qa + 2 * kk), B2 = lds_u2(qb + 2 * kk);
                     const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
                     P2 da, dl;
                     pair_values2<FAM, ST, PC, ZC>(p, q, kp, da, dl);
@@ -667,25 +685,13 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     if (tid == 0) s_nflag = 0;
 
     // ---- stage 0: region staging + per-pixel normalisation ----------------
-    // Record position c writes the first half of element c and the second
-    // half of element c-1.  Pad positions hold a neutral gray pixel; tiles
-    // whose region lies inside the image skip the border resolution.
-    auto put = [&](int pos, float gx, float gy, float gz, float aux, bool has_prev) {
-        float *ea = reinterpret_cast<float *>(sA + pos), *eb = reinterpret_cast<float *>(sB + pos);
-        ea[0] = gx; ea[2] = gy; eb[0] = gz; eb[2] = aux;
-        if (has_prev) {
-            ea[-4 + 1] = gx; ea[-4 + 3] = gy; eb[-4 + 1] = gz; eb[-4 + 3] = aux;
-        }
-    };
-    {
-        constexpr int NPAD = RWS - RW;
-        const float pad_aux = (ST == ST_MINIMAX) ? 0.57735026f : (ST == ST_CHROMA ? (1.f / 3.f) : 0.f);
-        for (int idx = tid; idx < RH * NPAD; idx += NT) {
-            const int ry = idx / NPAD, k = idx - ry * NPAD;
-            const int c = k < PADC ? k : RW + k;
-            put(ry * RWS + c, 1.f, 1.f, 1.f, pad_aux, c > 0);
-        }
-    }
+    // Pass 1 normalises every region pixel into a temporary float4 record
+    // (in the plane buffer, free at this point); pass 2 assembles the pair
+    // elements (c, c+1) with whole 16-byte stores.  Pad positions hold a
+    // neutral gray pixel; tiles inside the image skip the border resolution.
+    float4 *tmp = reinterpret_cast<float4 *>(sD);
+    static_assert((size_t)C::NPL * RN * sizeof(DT) >= (size_t)RN * sizeof(float4), "staging temp fits");
+    const float pad_aux = (ST == ST_MINIMAX) ? 0.57735026f : (ST == ST_CHROMA ? (1.f / 3.f) : 0.f);
     const int gy_top = kp.out_row0 + tile_y0 - H;  // global row of region row 0
     const bool inside = gy_top >= kp.in_row0 && gy_top + RH <= kp.in_row0 + kp.in_rows &&
                         gy_top >= 0 && gy_top + RH <= kp.global_H && tile_x0 - H >= 0 && tile_x0 - H + RW <= kp.W;
@@ -711,11 +717,21 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         if (ST == ST_CHROMA) aux = __frcp_rn(gx + gy + gz);
         aux = __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
         sK[idx] = r8 | (g8 << 8) | (b8 << 16);
-        put(ry * RWS + PADC + rx, gx, gy, gz, aux, true);
+        tmp[idx] = make_float4(gx, gy, gz, aux);
     }
     // zero vectors (raw 0 vs gray-mapped 1) only matter to the Minkowski term
-    const bool zany = __syncthreads_or(any_zero);  // also the staging barrier
+    const bool zany = __syncthreads_or(any_zero);  // also the pass-1 barrier
     const bool zchk = C::NEED_L && zany;
+    for (int idx = tid; idx < C::RECN; idx += NT) {
+        const int ry = idx / RWS, c = idx - ry * RWS;
+        const int r0 = c - PADC, r1 = r0 + 1;
+        const float4 neutral = make_float4(1.f, 1.f, 1.f, pad_aux);
+        const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
+        const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
+        sA[idx] = make_float4(f.x, s.x, f.y, s.y);
+        sB[idx] = make_float4(f.z, s.z, f.w, s.w);
+    }
+    __syncthreads();
 
     // aggregates: BOTH -> packed (angular, Minkowski) pairs; else scalars
     P2 ag[OPT][BOTH ? N : 1], cen[OPT][(BOTH && ACW) ? N : 1];
@@ -755,13 +771,13 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                         const int it = itg - i0;
                         const int py = it / RW, px = it - py * RW;
                         const int pidx = py * RWS + PADC + px;
-                        const float4 a4 = sA[pidx], b4 = sB[pidx];
+                        const float4 a4 = lds_f4(sA + pidx), b4 = lds_f4(sB + pidx);
                         const Pix p = {a4.x, a4.z, b4.x, b4.z};
                         const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
                         const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
     #pragma unroll
                         for (int kk = 0; kk < NK2; kk++) {
-                            const ulonglong2 A2 = qa[2 * kk], B2 = qb[2 * kk];
+                            const ulonglong2 A2 = lds_u2(qa + 2 * kk), B2 = lds_u2(qb + 2 * kk);
                             const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
                             P2 da, dl;
                             pair_values2<FAM, ST, PC, ZC>(p, q, kp, da, dl);

@@ -149,8 +149,8 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
             Pair2 pp[7];
 #pragma unroll
             for (int t = 0; t < 7; t++) {
-                const ulonglong2 A2 = reinterpret_cast<const ulonglong2 *>(rA + rsl[t] * C::LANES_E)[els[t]];
-                const ulonglong2 B2 = reinterpret_cast<const ulonglong2 *>(rB + rsl[t] * C::LANES_E)[els[t]];
+                const ulonglong2 A2 = lds_u2(rA + rsl[t] * C::LANES_E + els[t]);
+                const ulonglong2 B2 = lds_u2(rB + rsl[t] * C::LANES_E + els[t]);
                 pp[t] = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
             }
             P2 da[7], dl[7];
