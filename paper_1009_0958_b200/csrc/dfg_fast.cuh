@@ -440,6 +440,109 @@ struct Sel {
     }
 };
 
+// Window selection in two passes (cheaper than Sel's single pass):
+//   1. first strict minimum v1 (window order, like the reference's argmin)
+//      with its index, colour and optional payload;
+//   2. the smallest value among candidates of a different colour.
+// val(ic), col(ic), pa(ic), pl(ic) take std::integral_constant indices so the
+// caller's register arrays stay compile-time indexed.
+struct Pick {
+    float v1, other, xa, xl;
+    int i1;
+    uint32_t k1;
+    // FP32 order of winner and competitor not certain under the bound
+    // er*|v| + ea*lmax per candidate (no competitor: inf - inf = NaN -> false)
+    __device__ __forceinline__ bool doubtful(float er, float ea_lmax) const
+    {
+        return (other - v1) - er * fabsf(other) <= er * fabsf(v1) + 2.f * ea_lmax;
+    }
+};
+
+template <int N, bool PAY, typename FV, typename FC, typename FA, typename FL>
+__device__ __forceinline__ Pick pick(FV val, FC col, FA pa, FL pl)
+{
+    Pick r;
+    r.v1 = val(std::integral_constant<int, 0>{});
+    r.i1 = 0;
+    r.k1 = col(std::integral_constant<int, 0>{});
+    if constexpr (PAY) {
+        r.xa = pa(std::integral_constant<int, 0>{});
+        r.xl = pl(std::integral_constant<int, 0>{});
+    }
+    static_for<1, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        const float v = val(ic);
+        const bool p = v < r.v1;
+        r.v1 = p ? v : r.v1;
+        r.i1 = p ? i : r.i1;
+        r.k1 = p ? col(ic) : r.k1;
+        if constexpr (PAY) {
+            r.xa = p ? pa(ic) : r.xa;
+            r.xl = p ? pl(ic) : r.xl;
+        }
+    });
+    r.other = __int_as_float(0x7f800000);
+    static_for<0, N>([&](auto ic) {
+        if (col(ic) != r.k1) r.other = fminf(r.other, val(ic));
+    });
+    return r;
+}
+
+// The reference's selection for one output (E:317-355, E:451-487) on the
+// FP32 aggregates: A(ic)/L(ic) angular/Minkowski aggregates, AD/LD the
+// ACWDDF centre column, col(ic) the candidate colours.  Returns the chosen
+// window index and whether the decision is within the FP32 error budget.
+template <int FAM, int ST, int N, int DC, typename FA, typename FL, typename FAD, typename FLD, typename FC>
+__device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD AD, FLD LD, FC col, int &b,
+                                              bool &doubt)
+{
+    const float er = kp.er, ea = kp.ea;
+    auto none = [](auto) { return 0.f; };
+    if constexpr (FAM == FAM_ACWDDF) {
+        const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
+        float lmax = 0.f;  // largest Minkowski factor of any product (w0 >= w1 >= w2 >= 0)
+        static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, fmaf(w0, LD(ic), L(ic))); });
+        const Pick sd = pick<N, false>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
+        const Pick s0 = pick<N, true>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
+                                      col, AD, LD);
+        const Pick s1 = pick<N, true>([&](auto ic) { return fmaf(w1, AD(ic), A(ic)) * fmaf(w1, LD(ic), L(ic)); },
+                                      col, AD, LD);
+        const Pick s2 = pick<N, true>([&](auto ic) { return fmaf(w2, AD(ic), A(ic)) * fmaf(w2, LD(ic), L(ic)); },
+                                      col, AD, LD);
+        float a = s0.xa;
+        if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
+        float sv = a * s0.xl;
+        a = s1.xa;
+        if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
+        sv = fmaf(a, s1.xl, sv);
+        a = s2.xa;
+        if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
+        sv = fmaf(a, s2.xl, sv);
+        const float ld_sum = s0.xl + s1.xl + s2.xl;
+        const float es = 4.f * er * fmaxf(fabsf(sv), kp.threshold) +
+                         2.f * kp.ea_pair * (ST == ST_CHROMA ? kp.slope : 1.f) * ld_sum + 1e-6f;
+        const bool fires = sv > kp.threshold;
+        b = fires ? sd.i1 : DC;
+        const float er2 = 2.f * er, eal = 2.f * ea * lmax;
+        doubt = s0.doubtful(er2, eal) || s1.doubtful(er2, eal) || s2.doubtful(er2, eal) ||
+                fabsf(sv - kp.threshold) <= es || (fires && sd.doubtful(er2, eal));
+    } else if constexpr (FAM == FAM_DDF) {
+        float lmax = 0.f;
+        static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, L(ic)); });
+        const Pick s = pick<N, false>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
+        b = s.i1;
+        doubt = s.doubtful(2.f * er, 2.f * ea * lmax);
+    } else if constexpr (FAM == FAM_BVDF) {
+        const Pick s = pick<N, false>(A, col, none, none);
+        b = s.i1;
+        doubt = s.doubtful(er, ea);
+    } else {
+        const Pick s = pick<N, false>(L, col, none, none);
+        b = s.i1;
+        doubt = s.doubtful(er, 0.f);
+    }
+}
+
 // Two pairs (p, q) and (p, q+1): angular and/or Minkowski distances.
 template <int FAM, int ST, int PC, bool ZC>
 __device__ __forceinline__ void pair_values2(const Pix &p, const Pair2 &q, const KParams &kp, P2 &da, P2 &dl)
@@ -848,7 +951,6 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     });
 
     // ---- stage 3: selection ------------------------------------------------
-    const float er = kp.er, ea = kp.ea;
     const int ox = tile_x0 + tx;
 #pragma unroll
     for (int o = 0; o < OPT; o++) {
@@ -857,68 +959,26 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         const bool valid = (oy < kp.out_rows) && (ox < kp.W);
         int b;
         bool doubt;
-        if constexpr (ACW) {
-            Sel sd, s0, s1, s2;
-            const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                const uint32_t col = sK[(ry0 + i / S) * RW + tx + i % S];
-                const float a = lo2(ag[o][i]), l = hi2(ag[o][i]);
-                const float ad = lo2(cen[o][i]), ld = hi2(cen[o][i]);
-                const float pd = a * l;
-                const float l0 = fmaf(w0, ld, l), l1 = fmaf(w1, ld, l), l2 = fmaf(w2, ld, l);
-                const float p0 = fmaf(w0, ad, a) * l0, p1 = fmaf(w1, ad, a) * l1, p2 = fmaf(w2, ad, a) * l2;
-                if (i == 0) {
-                    sd.init(pd, l, col, 0.f, 0.f);
-                    s0.init(p0, l0, col, ad, ld);
-                    s1.init(p1, l1, col, ad, ld);
-                    s2.init(p2, l2, col, ad, ld);
-                } else {
-                    sd.add(pd, l, i, col, 0.f, 0.f);
-                    s0.add(p0, l0, i, col, ad, ld);
-                    s1.add(p1, l1, i, col, ad, ld);
-                    s2.add(p2, l2, i, col, ad, ld);
-                }
+        {
+            auto col = [&](auto ic) {
+                constexpr int i = decltype(ic)::value;
+                return sK[(ry0 + i / S) * RW + tx + i % S];
+            };
+            if constexpr (BOTH) {
+                auto A = [&](auto ic) { return lo2(ag[o][decltype(ic)::value]); };
+                auto L = [&](auto ic) { return hi2(ag[o][decltype(ic)::value]); };
+                auto AD = [&](auto ic) { if constexpr (ACW) return lo2(cen[o][decltype(ic)::value]); else return 0.f; };
+                auto LD = [&](auto ic) { if constexpr (ACW) return hi2(cen[o][decltype(ic)::value]); else return 0.f; };
+                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, b, doubt);
+            } else if constexpr (C::NEED_A) {
+                auto V = [&](auto ic) { return aA[o][decltype(ic)::value]; };
+                auto Z = [](auto) { return 0.f; };
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, b, doubt);
+            } else {
+                auto V = [&](auto ic) { return aL[o][decltype(ic)::value]; };
+                auto Z = [](auto) { return 0.f; };
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, b, doubt);
             }
-            float a = s0.xa;
-            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
-            float sv = a * s0.xl;
-            a = s1.xa;
-            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
-            sv = fmaf(a, s1.xl, sv);
-            a = s2.xa;
-            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
-            sv = fmaf(a, s2.xl, sv);
-            const float ld_sum = s0.xl + s1.xl + s2.xl;
-            const float es = 4.f * er * fmaxf(fabsf(sv), kp.threshold) +
-                             2.f * kp.ea_pair * (ST == ST_CHROMA ? kp.slope : 1.f) * ld_sum + 1e-6f;
-            const bool fires = sv > kp.threshold;
-            b = fires ? sd.i1 : DC;
-            const float er2 = 2.f * er, ea2 = 2.f * ea;
-            doubt = s0.doubtful(er2, ea2) || s1.doubtful(er2, ea2) || s2.doubtful(er2, ea2) ||
-                    fabsf(sv - kp.threshold) <= es || (fires && sd.doubtful(er2, ea2));
-        } else {
-            // BVDF: bound er|v| + ea (l = 1); VMF: er v (l = 0); DDF: 2er|v| + 2ea l
-            Sel sl;
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                const uint32_t col = sK[(ry0 + i / S) * RW + tx + i % S];
-                float v, l;
-                if constexpr (FAM == FAM_BVDF) {
-                    v = aA[o][i];
-                    l = 1.f;
-                } else if constexpr (FAM == FAM_VMF) {
-                    v = aL[o][i];
-                    l = 0.f;
-                } else {
-                    l = hi2(ag[o][i]);
-                    v = lo2(ag[o][i]) * l;
-                }
-                if (i == 0) sl.init(v, l, col, 0.f, 0.f);
-                else sl.add(v, l, i, col, 0.f, 0.f);
-            }
-            b = sl.i1;
-            doubt = (FAM == FAM_DDF) ? sl.doubtful(2.f * er, 2.f * ea) : sl.doubtful(er, ea);
         }
 
         if (kp.dbg != nullptr && valid) {

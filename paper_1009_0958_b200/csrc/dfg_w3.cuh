@@ -74,7 +74,6 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
     const int colr = resolve_idx(col, kp.W, kp.border);
     const int oy0 = chunk * rows_per_chunk;  // first output row (strip-local) of the chunk
     const int oy1 = min(kp.out_rows, oy0 + rows_per_chunk);
-    const float er = kp.er, ea = kp.ea;
 
     // pad elements (lanes 32, 33) of every ring row: neutral, never used
     if (lane < 2) {
@@ -106,20 +105,21 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         if (y < oy1) load_px(y + 1, nr8, ng8, nb8);
         const bool zero = (r8 | g8 | b8) == 0;
         Pix q;
-        q.x = zero ? 1.f : (float)r8;
-        q.y = zero ? 1.f : (float)g8;
-        q.z = zero ? 1.f : (float)b8;
+        // exact u8 -> float without I2F: 2^23 + v, minus 2^23
+        q.x = zero ? 1.f : __uint_as_float(0x4B000000u | r8) - 8388608.f;
+        q.y = zero ? 1.f : __uint_as_float(0x4B000000u | g8) - 8388608.f;
+        q.z = zero ? 1.f : __uint_as_float(0x4B000000u | b8) - 8388608.f;
         float aux = 0.f;
         if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(q.z, q.z, fmaf(q.y, q.y, q.x * q.x)));
         if (ST == ST_CHROMA) aux = __frcp_rn(q.x + q.y + q.z);
         q.aux = __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
         {
-            float *ea4 = reinterpret_cast<float *>(rA + slot * C::LANES_E + lane);
-            float *eb4 = reinterpret_cast<float *>(rB + slot * C::LANES_E + lane);
-            ea4[0] = q.x; ea4[2] = q.y; eb4[0] = q.z; eb4[2] = q.aux;
-            if (lane > 0) {
-                ea4[-4 + 1] = q.x; ea4[-4 + 3] = q.y; eb4[-4 + 1] = q.z; eb4[-4 + 3] = q.aux;
-            }
+            // element l = pixel pair (l, l+1): the right neighbour's record by
+            // shuffle, two whole 16-byte stores (lane 31's second half: unused)
+            const float sx = __shfl_down_sync(0xffffffffu, q.x, 1), sy = __shfl_down_sync(0xffffffffu, q.y, 1);
+            const float sz = __shfl_down_sync(0xffffffffu, q.z, 1), sa = __shfl_down_sync(0xffffffffu, q.aux, 1);
+            rA[slot * C::LANES_E + lane] = make_float4(q.x, sx, q.y, sy);
+            rB[slot * C::LANES_E + lane] = make_float4(q.z, sz, q.aux, sa);
             rK[slot * 32 + lane] = r8 | (g8 << 8) | (b8 << 16);
         }
         const bool zr2 = __any_sync(0xffffffffu, zero);
@@ -218,65 +218,19 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         for (int i = 0; i < N; i++) wc[i] = kR[i / 3][i % 3];
         int b;
         bool doubt;
-        if constexpr (ACW) {
-            Sel sd, s0, s1, s2;
-            const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                const float a = lo2(ag[i]), l = hi2(ag[i]);
-                const float ad = lo2(cen[i]), ld = hi2(cen[i]);
-                const float pd = a * l;
-                const float l0 = fmaf(w0, ld, l), l1 = fmaf(w1, ld, l), l2 = fmaf(w2, ld, l);
-                const float p0 = fmaf(w0, ad, a) * l0, p1 = fmaf(w1, ad, a) * l1, p2 = fmaf(w2, ad, a) * l2;
-                if (i == 0) {
-                    sd.init(pd, l, wc[i], 0.f, 0.f);
-                    s0.init(p0, l0, wc[i], ad, ld);
-                    s1.init(p1, l1, wc[i], ad, ld);
-                    s2.init(p2, l2, wc[i], ad, ld);
-                } else {
-                    sd.add(pd, l, i, wc[i], 0.f, 0.f);
-                    s0.add(p0, l0, i, wc[i], ad, ld);
-                    s1.add(p1, l1, i, wc[i], ad, ld);
-                    s2.add(p2, l2, i, wc[i], ad, ld);
-                }
+        {
+            auto col = [&](auto ic) { return wc[decltype(ic)::value]; };
+            if constexpr (BOTH) {
+                auto A = [&](auto ic) { return lo2(ag[decltype(ic)::value]); };
+                auto L = [&](auto ic) { return hi2(ag[decltype(ic)::value]); };
+                auto AD = [&](auto ic) { if constexpr (ACW) return lo2(cen[decltype(ic)::value]); else return 0.f; };
+                auto LD = [&](auto ic) { if constexpr (ACW) return hi2(cen[decltype(ic)::value]); else return 0.f; };
+                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, b, doubt);
+            } else {
+                auto V = [&](auto ic) { return aS[decltype(ic)::value]; };
+                auto Z = [](auto) { return 0.f; };
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, b, doubt);
             }
-            float a = s0.xa;
-            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
-            float sv = a * s0.xl;
-            a = s1.xa;
-            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
-            sv = fmaf(a, s1.xl, sv);
-            a = s2.xa;
-            if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
-            sv = fmaf(a, s2.xl, sv);
-            const float ld_sum = s0.xl + s1.xl + s2.xl;
-            const float es = 4.f * er * fmaxf(fabsf(sv), kp.threshold) +
-                             2.f * kp.ea_pair * (ST == ST_CHROMA ? kp.slope : 1.f) * ld_sum + 1e-6f;
-            const bool fires = sv > kp.threshold;
-            b = fires ? sd.i1 : DC;
-            const float er2 = 2.f * er, ea2 = 2.f * ea;
-            doubt = s0.doubtful(er2, ea2) || s1.doubtful(er2, ea2) || s2.doubtful(er2, ea2) ||
-                    fabsf(sv - kp.threshold) <= es || (fires && sd.doubtful(er2, ea2));
-        } else {
-            Sel sl;
-#pragma unroll
-            for (int i = 0; i < N; i++) {
-                float v, l;
-                if constexpr (FAM == FAM_BVDF) {
-                    v = aS[i];
-                    l = 1.f;
-                } else if constexpr (FAM == FAM_VMF) {
-                    v = aS[i];
-                    l = 0.f;
-                } else {
-                    l = hi2(ag[i]);
-                    v = lo2(ag[i]) * l;
-                }
-                if (i == 0) sl.init(v, l, wc[i], 0.f, 0.f);
-                else sl.add(v, l, i, wc[i], 0.f, 0.f);
-            }
-            b = sl.i1;
-            doubt = (FAM == FAM_DDF) ? sl.doubtful(2.f * er, 2.f * ea) : sl.doubtful(er, ea);
         }
         uint8_t *orow = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch;
         if (kp.dbg != nullptr && valid) {
