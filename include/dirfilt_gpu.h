@@ -119,9 +119,9 @@ DFG_API int dfg_filter_batch(const uint8_t *d_in, int32_t B, int32_t H, int32_t 
                      const dfg_params *prm, void *d_workspace, size_t workspace_bytes,
                      void *stream);
 
-/* End to end from HOST memory (pinned or pageable): H2D, filter, D2H on
- * `stream`, synchronised before return.  Device buffers are cached per
- * calling thread and grown on demand. */
+/* End to end from HOST memory (pinned or pageable), synchronised before
+ * return: cached per-thread device buffers and a row-band H2D / kernel /
+ * D2H pipeline on `stream` and two copy streams (pinned buffers overlap). */
 DFG_API int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out,
                     const dfg_params *prm, void *stream);
 

@@ -283,6 +283,28 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
         c.px_cap = px;
         c.dev = dev;
     }
+    // Opt-in (DFG_HOST_ZEROCOPY=1) for pinned, device-mapped host buffers:
+    // zero-copy -- the kernel reads its input and writes its output over
+    // PCIe directly, one launch.  Measured slower than the banded copies
+    // below for every config (byte-granular PCIe reads, halo re-reads), so
+    // off by default.
+    static const bool zc_env = [] {
+        const char *e = getenv("DFG_HOST_ZEROCOPY");
+        return e && e[0] == '1';
+    }();
+    if (zc_env) {
+        cudaPointerAttributes ai, ao;
+        if (cudaPointerGetAttributes(&ai, h_in) == cudaSuccess && cudaPointerGetAttributes(&ao, h_out) == cudaSuccess &&
+            ai.type == cudaMemoryTypeHost && ao.type == cudaMemoryTypeHost && ai.devicePointer && ao.devicePointer) {
+            rc = run((const uint8_t *)ai.devicePointer, H, W, 0, H, 3LL * W, 0, (uint8_t *)ao.devicePointer, 0, H,
+                     3LL * W, 0, 1, prm, c.ws, dfg_workspace_bytes((int64_t)px), stream, nullptr);
+            if (rc) return rc;
+            cudaError_t e = cudaStreamSynchronize(st);
+            if (e != cudaSuccess) return cuda_fail(e, "synchronize");
+            return DFG_OK;
+        }
+        cudaGetLastError();  // pageable memory: clear the attribute query's error state
+    }
     // Row-band pipeline: H2D of band k+1 (copy engine 1), the kernel of band
     // k (on `stream`) and D2H of band k-1 (copy engine 2) overlap.  Band k's
     // kernel waits for the input rows its windows reach (k+1's first rows).

@@ -312,8 +312,13 @@ cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KP
     // rows per chunk: about one wave of resident warps (16 per SM), more
     // rows (fewer warm-up rows, 2 per chunk) when the input is taller
     const long long strip_rows = (long long)n_strips * kp.out_rows * kp.n_frames;
+    static const int rpc_env = [] {
+        const char *e = getenv("DFG_W3_RPC");  // diagnostics only
+        return e ? atoi(e) : 0;
+    }();
     int rpc = (int)(strip_rows / (148 * 16));
     rpc = rpc < 16 ? 16 : (rpc > 64 ? 64 : rpc);
+    if (rpc_env > 0) rpc = rpc_env;
     const int n_chunks = (kp.out_rows + rpc - 1) / rpc;
     const int warps = n_strips * n_chunks;
     dim3 grid((warps + C::WARPS - 1) / C::WARPS, 1, kp.n_frames);
