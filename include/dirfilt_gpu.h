@@ -142,6 +142,31 @@ DFG_API int dfg_debug_values(const uint8_t *d_in, int32_t H, int32_t W, int64_t 
  * perturb_ulps and refines. */
 DFG_API double dfg_cr_acos_host(double z, int32_t perturb_ulps);
 
+/* Correlated impulsive noise (paper Eq. 8) -- replaces corrupt_image
+ * (reference noise.py:85-116).  The generator is numpy's PCG64 as seeded by
+ * np.random.PCG64(seed): the caller passes its initial 128-bit state and
+ * increment (bit_generator.state), and the device draws the same five
+ * doubles per pixel in row-major order, so the output equals the
+ * reference's bit for bit.  impulse: 0 = saltpepper, 1 = uniform. */
+typedef struct dfg_noise_params {
+    double phi, phi1, phi2, phi3;
+    int32_t impulse;
+    int32_t reserved;
+    uint64_t state_hi, state_lo, inc_hi, inc_lo;
+} dfg_noise_params;
+
+DFG_API int dfg_corrupt_image(const uint8_t *d_in, int32_t H, int32_t W, int64_t in_pitch,
+                      uint8_t *d_out, int64_t out_pitch, const dfg_noise_params *np,
+                      void *stream);
+
+/* Effectiveness criteria of reference metrics.py:64-109 (compare()):
+ * out3 = {MAE, PSNR [dB] (inf when identical), NCD x 1000} of d_test
+ * against d_ref, float64 sums on the device.  d_scratch: >= 32 bytes of
+ * device memory.  Synchronises `stream` before returning. */
+DFG_API int dfg_image_metrics(const uint8_t *d_ref, const uint8_t *d_test, int32_t H, int32_t W,
+                      int64_t ref_pitch, int64_t test_pitch, double *out3, void *d_scratch,
+                      void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,8 @@ from .filters import (
     fixup_counts,
     last_fixup_count,
 )
+from .metrics import MetricsReport, compare, mae, metrics_device, ncd, psnr
+from .noise import NoiseParams, corrupt_device, corrupt_image
 from .image import REFLECT, REPLICATE, BorderPolicy, ColorVector, RasterImage, to_uint8
 from .spec import (
     ACOS_COEFFICIENTS,
@@ -41,4 +43,6 @@ __all__ = [
     "FAMILIES", "FastAcosTable", "FilterSpec", "MinimaxPoly", "REFLECT", "REPLICATE",
     "RasterImage", "apply_filter", "center_weight", "filter_batch_device", "filter_device",
     "filter_host", "filter_rows_device", "fixup_counts", "last_fixup_count", "parse_filter_spec", "to_uint8",
+    "MetricsReport", "compare", "mae", "psnr", "ncd", "metrics_device",
+    "NoiseParams", "corrupt_device", "corrupt_image",
 ]

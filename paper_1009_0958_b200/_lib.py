@@ -20,7 +20,8 @@ BORDER_CODE = {"replicate": 0, "reflect": 1}
 EXPORTS = (
     "dfg_abi_version", "dfg_last_error", "dfg_workspace_bytes", "dfg_filter",
     "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_fixup_count",
-    "dfg_reset_counts", "dfg_debug_values", "dfg_cr_acos_host",
+    "dfg_reset_counts", "dfg_debug_values", "dfg_cr_acos_host", "dfg_corrupt_image",
+    "dfg_image_metrics",
 )
 
 
@@ -38,6 +39,21 @@ class DfgParams(ctypes.Structure):
         ("threshold", ctypes.c_double),
         ("slope", ctypes.c_double),
         ("intercept", ctypes.c_double),
+    ]
+
+
+class DfgNoiseParams(ctypes.Structure):
+    _fields_ = [
+        ("phi", ctypes.c_double),
+        ("phi1", ctypes.c_double),
+        ("phi2", ctypes.c_double),
+        ("phi3", ctypes.c_double),
+        ("impulse", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("state_hi", ctypes.c_uint64),
+        ("state_lo", ctypes.c_uint64),
+        ("inc_hi", ctypes.c_uint64),
+        ("inc_lo", ctypes.c_uint64),
     ]
 
 
@@ -68,8 +84,11 @@ def lib() -> ctypes.CDLL:
     L.dfg_debug_values.argtypes = [vp, i32, i32, i64, vp, P, vp]
     L.dfg_cr_acos_host.argtypes = [ctypes.c_double, i32]
     L.dfg_cr_acos_host.restype = ctypes.c_double
+    L.dfg_corrupt_image.argtypes = [vp, i32, i32, i64, vp, i64, ctypes.POINTER(DfgNoiseParams), vp]
+    L.dfg_image_metrics.argtypes = [vp, vp, i32, i32, i64, i64, ctypes.POINTER(ctypes.c_double), vp, vp]
     for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host",
-                 "dfg_fixup_count", "dfg_reset_counts", "dfg_debug_values"):
+                 "dfg_fixup_count", "dfg_reset_counts", "dfg_debug_values", "dfg_corrupt_image",
+                 "dfg_image_metrics"):
         getattr(L, name).restype = ctypes.c_int
     if L.dfg_abi_version() != 1:
         raise RuntimeError("libdfg.so ABI version mismatch; rebuild")

@@ -23,6 +23,12 @@ def golden():
 
 
 @pytest.fixture(scope="session")
+def golden_full():
+    """Same fixtures with the whole manifest (noise cases, metrics pairs)."""
+    return np.load(GOLDEN / "filters.npz"), json.loads((GOLDEN / "manifest.json").read_text())
+
+
+@pytest.fixture(scope="session")
 def cuda():
     import torch
 

@@ -32,7 +32,7 @@ sys.path.insert(0, str(REPO))
 
 import dirfilt  # noqa: E402  (the reference)
 from dirfilt import (  # noqa: E402
-    BorderPolicy, NoiseParams, RasterImage, apply_filter, corrupt_image, parse_filter_spec,
+    BorderPolicy, NoiseParams, RasterImage, apply_filter, compare, corrupt_image, parse_filter_spec,
 )
 from dirfilt.distance import (  # noqa: E402
     FastAcosTable, angular_distance_exact, chromaticity_distance, minkowski_distance,
@@ -140,9 +140,37 @@ def main() -> None:
     arrays["noise_clean"] = clean
     arrays["noise_ref"] = noisy.pixels.astype(np.uint8)
 
+    # the full simulator: both impulse modes, all four branches, a pixel
+    # count that is not a multiple of the device's 16-pixel runs
+    noise_cases = [
+        ("sp_default", (37, 53), dict(seed=7)),
+        ("uni_mixed", (41, 61), dict(phi=0.5, phi1=0.1, phi2=0.2, phi3=0.3, impulse="uniform", seed=123456789)),
+        ("sp_all", (9, 7), dict(phi=1.0, phi1=0.0, phi2=0.0, phi3=0.0, seed=2**63 + 5)),
+        ("sp_branch3", (16, 33), dict(phi=0.9, phi1=0.0, phi2=0.0, phi3=1.0, seed=0)),
+    ]
+    noise_manifest = []
+    for name, (h, w), kw in noise_cases:
+        img = synth.clean_image(h, w, len(noise_manifest) + 40)
+        out = corrupt_image(RasterImage(img.astype(np.float64)), NoiseParams(**kw)).pixels
+        arrays[f"noise_{name}_in"] = img
+        arrays[f"noise_{name}_out"] = out.astype(np.uint8)
+        noise_manifest.append({"name": name, **kw})
+
+    # effectiveness criteria (metrics.py:64-118) on a few image pairs
+    pairs = [("noise_clean", "noise_ref"), ("noise_sp_default_in", "noise_sp_default_out"),
+             ("noise_uni_mixed_in", "noise_uni_mixed_out"), ("noise_clean", "noise_clean"),
+             ("in0", "out0")]
+    met = []
+    for a, b in pairs:
+        r = compare(RasterImage(arrays[a].astype(np.float64)), RasterImage(arrays[b].astype(np.float64)))
+        met.append([r.mae, r.psnr, r.ncd_x1000])
+    arrays["metrics_ref"] = np.asarray(met, dtype=np.float64)
+
     np.savez_compressed(HERE / "filters.npz", **arrays)
     (HERE / "manifest.json").write_text(json.dumps({"reference": "dirfilt 0.1.0 (/root/reference/pkg)",
-                                                    "numpy": np.__version__, "cases": cases}, indent=1))
+                                                    "numpy": np.__version__, "cases": cases,
+                                                    "noise_cases": noise_manifest,
+                                                    "metrics_pairs": pairs}, indent=1))
     print(f"{len(cases)} filter cases, {sum(a.nbytes for a in arrays.values())} bytes raw")
 
 

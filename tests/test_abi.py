@@ -41,6 +41,35 @@ def test_params_layout_matches_header(tmp_path):
     assert got == want
 
 
+def test_noise_params_layout_matches_header(tmp_path):
+    src = tmp_path / "nlayout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "dirfilt_gpu.h"\n'
+                   'int main(void){printf("%zu %zu %zu %zu\\n", sizeof(dfg_noise_params), '
+                   'offsetof(dfg_noise_params,impulse), offsetof(dfg_noise_params,state_hi), '
+                   'offsetof(dfg_noise_params,inc_lo));return 0;}\n')
+    exe = tmp_path / "nlayout"
+    subprocess.run(["gcc", f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    P = _lib.DfgNoiseParams
+    assert got == [ctypes.sizeof(P), P.impulse.offset, P.state_hi.offset, P.inc_lo.offset]
+
+
+def test_noise_and_metrics_validate_before_any_cuda_call():
+    """NoiseParams validation (reference noise.py:42-55) and dimension checks
+    are reported as DFG_E_ARG without touching the device."""
+    L = _lib.lib()
+    good = dict(phi=0.1, phi1=0.25, phi2=0.25, phi3=0.25, impulse=0)
+    for bad in (dict(phi=1.5), dict(phi=-0.1), dict(phi1=-0.01), dict(phi1=0.5, phi2=0.5, phi3=0.1),
+                dict(impulse=2)):
+        np_ = _lib.DfgNoiseParams(**{**good, **bad})
+        assert L.dfg_corrupt_image(ctypes.c_void_p(1), 4, 4, 12, ctypes.c_void_p(1), 12, ctypes.byref(np_), None) == -1
+    np_ = _lib.DfgNoiseParams(**good)
+    assert L.dfg_corrupt_image(ctypes.c_void_p(1), 0, 4, 12, ctypes.c_void_p(1), 12, ctypes.byref(np_), None) == -1
+    out = (ctypes.c_double * 3)()
+    assert L.dfg_image_metrics(ctypes.c_void_p(1), ctypes.c_void_p(1), 4, 4, 11, 12, out, ctypes.c_void_p(1),
+                               None) == -1
+
+
 @pytest.mark.parametrize("text,code", [("vmf:window=9", _lib.DFG_E_UNSUP), ("bvdf:exact:window=11", _lib.DFG_E_UNSUP)])
 def test_unsupported_window_reported_before_any_cuda_call(text, code):
     L = _lib.lib()
