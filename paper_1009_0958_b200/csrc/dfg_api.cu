@@ -135,7 +135,7 @@ cudaError_t launch_fast(const dfg_params *p, cudaStream_t st, const uint8_t *in,
 int run(const uint8_t *d_in, int global_H, int W, int in_row0, int in_rows, long long in_pitch,
         long long in_fstride, uint8_t *d_out, int out_row0, int out_rows, long long out_pitch,
         long long out_fstride, int frames, const dfg_params *prm, void *ws, size_t ws_bytes,
-        void *stream, float *dbg)
+        void *stream, float *dbg, int w3_rpc = 0, int hostio = 0)
 {
     int rc = validate(prm);
     if (rc) return rc;
@@ -182,23 +182,49 @@ int run(const uint8_t *d_in, int global_H, int W, int in_row0, int in_rows, long
     fill_params(prm, kp);
     kp.flag_count = (unsigned *)ws;
     kp.dbg = dbg;
+    kp.w3_rpc = w3_rpc;
+    kp.hostio = hostio;
 
     cudaError_t e = launch_fast(prm, st, d_in, d_out, kp);
     if (e != cudaSuccess) return cuda_fail(e, "fast kernel launch");
     return DFG_OK;
 }
 
-constexpr int kMaxBands = 8;
+constexpr int kMaxBands = 16;
+constexpr int kGraphs = 4;
+constexpr int kKStreams = 4;
+
+// One captured host-path pipeline (pinned buffers): replayed with a single
+// cudaGraphLaunch while the key matches.
+struct GraphEntry {
+    const uint8_t *h_in = nullptr;
+    uint8_t *h_out = nullptr;
+    int H = 0, W = 0, nb = 0;
+    dfg_params prm{};
+    cudaGraphExec_t exec = nullptr;
+    unsigned long long used = 0;
+};
 
 struct HostCache {
     uint8_t *d_in = nullptr, *d_out = nullptr;
     void *ws = nullptr;
     size_t px_cap = 0;
     int dev = -1;
-    cudaStream_t s_in = nullptr, s_out = nullptr;  // copy streams (H2D / D2H engines)
+    cudaStream_t s_in = nullptr, s_out = nullptr, s_cap = nullptr;  // copy streams (H2D / D2H engines), capture
+    cudaStream_t s_k[kKStreams] = {};                                // band kernels (overlapping)
     cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_in[kMaxBands] = {}, ev_k[kMaxBands] = {};
+    GraphEntry graphs[kGraphs];
+    unsigned long long tick = 0;
+    void drop_graphs()
+    {
+        for (GraphEntry &g : graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            g = GraphEntry();
+        }
+    }
     void release()
     {
+        drop_graphs();
         if (d_in) cudaFree(d_in);
         if (d_out) cudaFree(d_out);
         if (ws) cudaFree(ws);
@@ -248,6 +274,94 @@ int dfg_filter_batch(const uint8_t *d_in, int32_t B, int32_t H, int32_t W, int64
                ws, ws_bytes, stream, nullptr);
 }
 
+}  // extern "C"
+
+namespace {
+
+// Row-band pipeline: the H2D copies of all bands stream on one copy engine,
+// the D2H copies on the other (PCIe is full duplex), and band k's kernel runs
+// as soon as the input rows its windows reach (band k+1's first rows) have
+// landed.  Band kernels go round-robin to kKStreams streams so they overlap
+// each other as well as the copies; for 3x3 they use the warp row-sweep
+// kernel with short chunks (low latency per band; the SMs are otherwise idle
+// during the copies).  Fork and join are events on `st`, so the same sequence
+// is also capturable into a CUDA graph.
+int enqueue_bands(HostCache &c, const uint8_t *h_in, int H, int W, uint8_t *h_out, const dfg_params *prm,
+                  cudaStream_t st, int nb, int w3_rpc)
+{
+    const int h = (prm->family == DFG_IDENTITY) ? 0 : prm->window / 2;
+    const long long pitch = 3LL * W;
+    const size_t px = (size_t)H * W;
+    // band boundaries: geometric taper q (band k ~ q^k; q = 1: equal bands)
+    // -- later bands smaller, so the kernel + D2H tail after the last copy
+    // is short
+    static const double taper = [] {
+        const char *t = getenv("DFG_HOST_TAPER");  // diagnostics override
+        return t ? atof(t) : 1.0;
+    }();
+    auto row0 = [&](int k) {
+        if (k >= nb) return H;
+        if (taper == 1.0 || taper <= 0.0) return (int)((long long)k * H / nb);
+        return (int)(H * (1.0 - pow(taper, k)) / (1.0 - pow(taper, nb)));
+    };
+    const int nks = nb < kKStreams ? nb : kKStreams;
+    cudaError_t e = cudaEventRecord(c.ev_start, st);  // buffers are free once prior work on `st` is done
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_in, c.ev_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_out, c.ev_start, 0);
+    for (int k = 0; k < nks && e == cudaSuccess; k++) e = cudaStreamWaitEvent(c.s_k[k], c.ev_start, 0);
+    // band k's copy includes the h halo rows below it (rows the next band
+    // copies again -- identical bytes), so its kernel depends on its own
+    // copy only; the halo above arrived with the earlier bands
+    for (int k = 0; k < nb && e == cudaSuccess; k++) {
+        const int r0 = row0(k), r1 = row0(k + 1);
+        const int c0 = k == 0 ? 0 : r0 + h, c1 = k + 1 == nb ? H : r1 + h;  // rows [c0, c1)
+        if (c1 > c0)
+            e = cudaMemcpyAsync(c.d_in + c0 * pitch, h_in + c0 * pitch, (size_t)(c1 - c0) * pitch,
+                                cudaMemcpyHostToDevice, c.s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(c.ev_in[k], c.s_in);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "H2D");
+    for (int k = 0; k < nb; k++) {
+        const int r0 = row0(k), r1 = row0(k + 1);
+        cudaStream_t sk = c.s_k[k % nks];
+        e = cudaStreamWaitEvent(sk, c.ev_in[k], 0);
+        if (e != cudaSuccess) return cuda_fail(e, "band dependency");
+        int rc = run(c.d_in, H, W, 0, H, pitch, 0, c.d_out + r0 * pitch, r0, r1 - r0, pitch, 0, 1, prm, c.ws,
+                     dfg_workspace_bytes((int64_t)px), sk, nullptr, nb > 1 ? w3_rpc : 0);
+        if (rc) return rc;
+        e = cudaEventRecord(c.ev_k[k], sk);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_out, c.ev_k[k], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(h_out + r0 * pitch, c.d_out + r0 * pitch, (size_t)(r1 - r0) * pitch,
+                                cudaMemcpyDeviceToHost, c.s_out);
+        if (e != cudaSuccess) return cuda_fail(e, "D2H");
+    }
+    e = cudaEventRecord(c.ev_done, c.s_out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_done, 0);  // join: later work on `st` sees the result
+    if (e != cudaSuccess) return cuda_fail(e, "join");
+    return DFG_OK;
+}
+
+bool is_pinned(const void *p)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // clear the query's error state
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+int env_int(const char *name, int dflt)
+{
+    const char *s = getenv(name);
+    return s ? atoi(s) : dflt;
+}
+
+}  // namespace
+
+extern "C" {
+
 int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, const dfg_params *prm,
                     void *stream)
 {
@@ -269,6 +383,9 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
         if (e == cudaSuccess && c.dev != dev) {
             e = cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking);
             if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s_cap, cudaStreamNonBlocking);
+            for (int k = 0; k < kKStreams && e == cudaSuccess; k++)
+                e = cudaStreamCreateWithFlags(&c.s_k[k], cudaStreamNonBlocking);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_done, cudaEventDisableTiming);
             for (int k = 0; k < kMaxBands && e == cudaSuccess; k++) {
@@ -283,73 +400,107 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
         c.px_cap = px;
         c.dev = dev;
     }
-    // Opt-in (DFG_HOST_ZEROCOPY=1) for pinned, device-mapped host buffers:
-    // zero-copy -- the kernel reads its input and writes its output over
-    // PCIe directly, one launch.  Measured slower than the banded copies
-    // below for every config (byte-granular PCIe reads, halo re-reads), so
-    // off by default.
-    static const bool zc_env = [] {
-        const char *e = getenv("DFG_HOST_ZEROCOPY");
-        return e && e[0] == '1';
-    }();
-    if (zc_env) {
+    const bool pinned = is_pinned(h_in) && is_pinned(h_out);
+    // Opt-in (DFG_HOST_STREAM=1) for 3x3 with pinned buffers: zero-copy
+    // streaming -- one launch of the warp row-sweep kernel reads the input
+    // rows from and writes the output rows to the mapped host buffers
+    // itself, as aligned words.  Measured slower than the banded copies
+    // below (1024^2: 263 us vs 140 us; kernel-issued partial-line writes to
+    // host memory run at ~17 GB/s), so off by default.
+    const bool stream_on = env_int("DFG_HOST_STREAM", 0) != 0;  // read per call (tests switch it)
+    if (stream_on && pinned && prm->window == 3 && prm->family != DFG_IDENTITY) {
         cudaPointerAttributes ai, ao;
         if (cudaPointerGetAttributes(&ai, h_in) == cudaSuccess && cudaPointerGetAttributes(&ao, h_out) == cudaSuccess &&
-            ai.type == cudaMemoryTypeHost && ao.type == cudaMemoryTypeHost && ai.devicePointer && ao.devicePointer) {
-            rc = run((const uint8_t *)ai.devicePointer, H, W, 0, H, 3LL * W, 0, (uint8_t *)ao.devicePointer, 0, H,
-                     3LL * W, 0, 1, prm, c.ws, dfg_workspace_bytes((int64_t)px), stream, nullptr);
+            ai.devicePointer && ao.devicePointer) {
+            // diagnostics: DFG_HOST_STREAM=2 streams the input only (output
+            // via device memory + one D2H copy), 3 the output only
+            const int mode = env_int("DFG_HOST_STREAM", 1);
+            const uint8_t *kin = (const uint8_t *)ai.devicePointer;
+            uint8_t *kout = (uint8_t *)ao.devicePointer;
+            cudaError_t e = cudaSuccess;
+            if (mode == 3) {
+                e = cudaMemcpyAsync(c.d_in, h_in, 3 * px, cudaMemcpyHostToDevice, st);
+                kin = c.d_in;
+            }
+            if (mode == 2) kout = c.d_out;
+            if (e != cudaSuccess) return cuda_fail(e, "H2D");
+            rc = run(kin, H, W, 0, H, 3LL * W, 0, kout, 0, H, 3LL * W, 0, 1, prm, c.ws,
+                     dfg_workspace_bytes((int64_t)px), stream, nullptr, 0, 1);
             if (rc) return rc;
-            cudaError_t e = cudaStreamSynchronize(st);
+            if (mode == 2) e = cudaMemcpyAsync(h_out, c.d_out, 3 * px, cudaMemcpyDeviceToHost, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) return cuda_fail(e, "synchronize");
             return DFG_OK;
         }
-        cudaGetLastError();  // pageable memory: clear the attribute query's error state
+        cudaGetLastError();
     }
-    // Row-band pipeline: H2D of band k+1 (copy engine 1), the kernel of band
-    // k (on `stream`) and D2H of band k-1 (copy engine 2) overlap.  Band k's
-    // kernel waits for the input rows its windows reach (k+1's first rows).
     const int h = (prm->family == DFG_IDENTITY) ? 0 : prm->window / 2;
-    static const int nb_env = [] {
-        const char *s = getenv("DFG_HOST_BANDS");  // diagnostics only
-        return s ? atoi(s) : 0;
-    }();
-    // each band costs ~25 us of API calls: bands only pay off when the
-    // copies they hide are larger than that (>= ~0.5 M pixels per band)
-    int nb = nb_env > 0 ? nb_env : (int)(px / (512 * 1024));
+    static const int nb_env = env_int("DFG_HOST_BANDS", 0);  // diagnostics only
+    static const bool graph_on = env_int("DFG_HOST_GRAPH", 1) != 0;
+    const bool use_graph = pinned && graph_on;
+    // Eager issue costs ~25 us of API calls per band, so bands only pay off
+    // above ~0.5 M pixels each; a replayed graph has no per-band host cost,
+    // but every copy still costs the copy engine ~5 us: measured best at
+    // 2-4 bands for 1024^2 (137-141 us vs 178 us unbanded), 4 for 4096^2.
+    int nb = nb_env > 0 ? nb_env : (int)(px / (use_graph ? 256 * 1024 : 512 * 1024));
+    if (nb_env <= 0 && nb > 8) nb = 8;
     if (nb > H / 64) nb = H / 64;
     nb = nb < 1 ? 1 : (nb > kMaxBands ? kMaxBands : nb);
     if (prm->border == DFG_REFLECT && H <= 4 * h) nb = 1;
-    const long long pitch = 3LL * W;
-    auto row0 = [&](int k) { return (int)((long long)k * H / nb); };
-    cudaError_t e = cudaEventRecord(c.ev_start, st);  // buffers are free once prior work on `stream` is done
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_in, c.ev_start, 0);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_out, c.ev_start, 0);
-    for (int k = 0; k < nb && e == cudaSuccess; k++) {
-        const int r0 = row0(k), r1 = row0(k + 1);
-        e = cudaMemcpyAsync(c.d_in + r0 * pitch, h_in + r0 * pitch, (size_t)(r1 - r0) * pitch,
-                            cudaMemcpyHostToDevice, c.s_in);
-        if (e == cudaSuccess) e = cudaEventRecord(c.ev_in[k], c.s_in);
+    static const int w3_rpc = env_int("DFG_HOST_W3_RPC", 8);  // diagnostics override
+    cudaError_t e;
+    if (use_graph) {
+        GraphEntry *g = nullptr, *victim = &c.graphs[0];
+        for (GraphEntry &x : c.graphs) {
+            if (x.exec && x.h_in == h_in && x.h_out == h_out && x.H == H && x.W == W && x.nb == nb &&
+                memcmp(&x.prm, prm, sizeof(dfg_params)) == 0) {
+                g = &x;
+                break;
+            }
+            if (!x.exec || x.used < victim->used) victim = &x;
+        }
+        if (!g) {
+            // capture the pipeline once: the kernels' attributes are set
+            // outside capture by an eager first call
+            if (victim->exec) cudaGraphExecDestroy(victim->exec);
+            *victim = GraphEntry();
+            rc = enqueue_bands(c, h_in, H, W, h_out, prm, c.s_cap, nb, w3_rpc);
+            if (rc) return rc;
+            e = cudaStreamSynchronize(c.s_cap);
+            if (e != cudaSuccess) return cuda_fail(e, "warm-up");
+            cudaGraph_t graph = nullptr;
+            e = cudaStreamBeginCapture(c.s_cap, cudaStreamCaptureModeThreadLocal);
+            if (e != cudaSuccess) return cuda_fail(e, "begin capture");
+            rc = enqueue_bands(c, h_in, H, W, h_out, prm, c.s_cap, nb, w3_rpc);
+            e = cudaStreamEndCapture(c.s_cap, &graph);
+            if (rc) {
+                if (graph) cudaGraphDestroy(graph);
+                return rc;
+            }
+            if (e != cudaSuccess) return cuda_fail(e, "end capture");
+            e = cudaGraphInstantiate(&victim->exec, graph, 0);
+            cudaGraphDestroy(graph);
+            if (e != cudaSuccess) {
+                victim->exec = nullptr;
+                return cuda_fail(e, "graph instantiate");
+            }
+            victim->h_in = h_in;
+            victim->h_out = h_out;
+            victim->H = H;
+            victim->W = W;
+            victim->nb = nb;
+            victim->prm = *prm;
+            g = victim;
+        }
+        g->used = ++c.tick;
+        e = cudaGraphLaunch(g->exec, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+        return DFG_OK;
     }
-    if (e != cudaSuccess) return cuda_fail(e, "H2D");
-    for (int k = 0; k < nb; k++) {
-        const int r0 = row0(k), r1 = row0(k + 1);
-        int need = 0;  // last band whose rows the windows of band k reach
-        while (need + 1 < nb && row0(need + 1) < r1 + h) need++;
-        e = cudaStreamWaitEvent(st, c.ev_in[need], 0);
-        if (e != cudaSuccess) return cuda_fail(e, "band dependency");
-        rc = run(c.d_in, H, W, 0, H, pitch, 0, c.d_out + r0 * pitch, r0, r1 - r0, pitch, 0, 1, prm, c.ws,
-                 dfg_workspace_bytes((int64_t)px), stream, nullptr);
-        if (rc) return rc;
-        e = cudaEventRecord(c.ev_k[k], st);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_out, c.ev_k[k], 0);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync(h_out + r0 * pitch, c.d_out + r0 * pitch, (size_t)(r1 - r0) * pitch,
-                                cudaMemcpyDeviceToHost, c.s_out);
-        if (e != cudaSuccess) return cuda_fail(e, "D2H");
-    }
-    e = cudaEventRecord(c.ev_done, c.s_out);
-    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_done, 0);  // later work on `stream` sees the result
-    if (e == cudaSuccess) e = cudaEventSynchronize(c.ev_done);
+    rc = enqueue_bands(c, h_in, H, W, h_out, prm, st, nb, w3_rpc);
+    if (rc) return rc;
+    e = cudaEventSynchronize(c.ev_done);
     if (e != cudaSuccess) return cuda_fail(e, "synchronize");
     return DFG_OK;
 }

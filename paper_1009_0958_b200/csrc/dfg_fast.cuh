@@ -304,6 +304,43 @@ __device__ __forceinline__ P2 angle_exact2(const Pix &p, const Pair2 &q)
     return pk2(c0 > d0 ? lo2(alt) : lo2(at), c1 > d1 ? hi2(alt) : hi2(at));
 }
 
+// 2 atan(t) for t in [0, 1]: atan01's polynomial with every coefficient
+// doubled (binary scaling: bit-identical to 2 * atan01(t)).
+__device__ __forceinline__ P2 atan01x2_2(P2 m)
+{
+    const P2 t = mul2(m, m);
+    P2 q = fma2(bc2(2.f * -0.0046935188584029675f), t, bc2(2.f * 0.0242534838616848f));
+    q = fma2(q, t, bc2(2.f * -0.05948825553059578f));
+    q = fma2(q, t, bc2(2.f * 0.09914451837539673f));
+    q = fma2(q, t, bc2(2.f * -0.14019551873207092f));
+    q = fma2(q, t, bc2(2.f * 0.19969739019870758f));
+    q = fma2(q, t, bc2(2.f * -0.33331993222236633f));
+    q = fma2(q, t, bc2(2.f * 0.9999998807907104f));
+    return mul2(m, q);
+}
+
+// Exact route by the half-angle identity, two pairs: theta = 2 atan(t) with
+// t = tan(theta / 2) = |a x b| / (|a||b| + a.b) in [0, 1] for non-negative
+// vectors (theta <= pi/2), evaluated as t = cc * rsqrt(cc * den^2): one MUFU,
+// no range reduction and no branch select.  aux = |x| (IEEE sqrt of the
+// exact integer norm; the zero-pixel flag is its sign bit, cleared under ZC).
+template <bool ZC>
+__device__ __forceinline__ P2 angle_half2(const Pix &p, const Pair2 &q)
+{
+    P2 dot, cc;
+    cross_dot2(p, q, dot, cc);
+    float pa = p.aux;
+    P2 qa = q.aux;
+    if constexpr (ZC) {
+        pa = fabsf(pa);
+        qa = pk2(fabsf(lo2(qa)), fabsf(hi2(qa)));
+    }
+    const P2 den = fma2(bc2(pa), qa, dot);  // |a||b| + a.b, one rounding
+    const P2 P = mul2(cc, mul2(den, den));
+    const P2 R = pk2(rsqrt_approx(fmaxf(lo2(P), 1e-30f)), rsqrt_approx(fmaxf(hi2(P), 1e-30f)));
+    return atan01x2_2(mul2(cc, R));  // cc = 0 (parallel) -> exactly 0
+}
+
 // minimax route, two pairs (angle_minimax per lane, incl. the seam check)
 __device__ __forceinline__ P2 angle_minimax2(const Pix &p, const Pair2 &q, const KParams &kp)
 {
@@ -355,12 +392,39 @@ __device__ __forceinline__ P2 l2_2(const Pix &p, const Pair2 &q)
     return pk2(sqrt_approx(lo2(ss)), sqrt_approx(hi2(ss)));
 }
 
-// Zero-pixel flag: bit 0 of the stored aux word (1 ulp of aux, inside the
-// error budget; the exact route stores the bare flag).
-__device__ __forceinline__ bool zflag(float aux) { return (__float_as_uint(aux) & 1u) != 0u; }
+// Per-pixel aux word of the gray-mapped vector g and the zero-pixel flag it
+// carries: exact route |g| (IEEE sqrt of the exact integer norm) with the
+// flag in the sign bit -- set only when the Minkowski term needs it (FLAG),
+// whose zero-check (ZC) pair path then takes |aux|; minimax 1/|g| and
+// chromaticity 1/sum(g) with the flag in bit 0 (1 ulp of aux, inside the
+// error budget).
+template <int ST>
+__device__ __forceinline__ uint32_t zbit()
+{
+    return ST == ST_EXACT ? 0x80000000u : 1u;
+}
+template <int ST, bool FLAG>
+__device__ __forceinline__ float encode_aux(float gx, float gy, float gz, bool zero)
+{
+    const float n2 = fmaf(gz, gz, fmaf(gy, gy, gx * gx));  // exact integer
+    if (ST == ST_EXACT) {
+        const float a = __fsqrt_rn(n2);
+        return (FLAG && zero) ? -a : a;
+    }
+    float aux = 0.f;
+    if (ST == ST_MINIMAX) aux = rsqrtf(n2);
+    if (ST == ST_CHROMA) aux = __frcp_rn(gx + gy + gz);
+    return __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
+}
+template <int ST>
+__device__ __forceinline__ bool zflag(float aux)
+{
+    return (__float_as_uint(aux) & zbit<ST>()) != 0u;
+}
+template <int ST>
 __device__ __forceinline__ float4 rawrec(float x, float y, float z, float aux)
 {
-    const bool zr = zflag(aux);
+    const bool zr = zflag<ST>(aux);
     return make_float4(zr ? 0.f : x, zr ? 0.f : y, zr ? 0.f : z, aux);
 }
 
@@ -493,7 +557,7 @@ __device__ __forceinline__ Pick pick(FV val, FC col, FA pa, FL pl)
 // ACWDDF centre column, col(ic) the candidate colours.  Returns the chosen
 // window index and whether the decision is within the FP32 error budget.
 template <int FAM, int ST, int N, int DC, typename FA, typename FL, typename FAD, typename FLD, typename FC>
-__device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD AD, FLD LD, FC col, int &b,
+__device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD AD, FLD LD, FC col, uint32_t &kc,
                                               bool &doubt)
 {
     const float er = kp.er, ea = kp.ea;
@@ -522,7 +586,7 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
         const float es = 4.f * er * fmaxf(fabsf(sv), kp.threshold) +
                          2.f * kp.ea_pair * (ST == ST_CHROMA ? kp.slope : 1.f) * ld_sum + 1e-6f;
         const bool fires = sv > kp.threshold;
-        b = fires ? sd.i1 : DC;
+        kc = fires ? sd.k1 : col(std::integral_constant<int, DC>{});
         const float er2 = 2.f * er, eal = 2.f * ea * lmax;
         doubt = s0.doubtful(er2, eal) || s1.doubtful(er2, eal) || s2.doubtful(er2, eal) ||
                 fabsf(sv - kp.threshold) <= es || (fires && sd.doubtful(er2, eal));
@@ -530,15 +594,15 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
         float lmax = 0.f;
         static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, L(ic)); });
         const Pick s = pick<N, false>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
-        b = s.i1;
+        kc = s.k1;
         doubt = s.doubtful(2.f * er, 2.f * ea * lmax);
     } else if constexpr (FAM == FAM_BVDF) {
         const Pick s = pick<N, false>(A, col, none, none);
-        b = s.i1;
+        kc = s.k1;
         doubt = s.doubtful(er, ea);
     } else {
         const Pick s = pick<N, false>(L, col, none, none);
-        b = s.i1;
+        kc = s.k1;
         doubt = s.doubtful(er, 0.f);
     }
 }
@@ -550,7 +614,7 @@ __device__ __forceinline__ void pair_values2(const Pix &p, const Pair2 &q, const
     constexpr bool NA = FAM != FAM_VMF;
     constexpr bool NL = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
     if (NA) {
-        if (ST == ST_EXACT) da = angle_exact2(p, q);
+        if (ST == ST_EXACT) da = angle_half2<ZC>(p, q);
         else if (ST == ST_MINIMAX) da = angle_minimax2(p, q, kp);
         else if (PC == PC_2) da = chroma2_l2(p, q);
         else {
@@ -563,13 +627,13 @@ __device__ __forceinline__ void pair_values2(const Pix &p, const Pair2 &q, const
     }
     if (NL) {
         const bool anyz =
-            ZC && ((__float_as_uint(p.aux) | __float_as_uint(lo2(q.aux)) | __float_as_uint(hi2(q.aux))) & 1u);
+            ZC && ((__float_as_uint(p.aux) | __float_as_uint(lo2(q.aux)) | __float_as_uint(hi2(q.aux))) & zbit<ST>());
         if (PC == PC_2 && !anyz) {
             dl = l2_2(p, q);
         } else {  // zero pixels (raw 0 vs gray-mapped 1) or p != 2: per lane on raw values
-            const float4 a = rawrec(p.x, p.y, p.z, p.aux);
-            dl = pk2(minkowski<PC>(a, rawrec(lo2(q.x), lo2(q.y), lo2(q.z), lo2(q.aux)), kp),
-                     minkowski<PC>(a, rawrec(hi2(q.x), hi2(q.y), hi2(q.z), hi2(q.aux)), kp));
+            const float4 a = rawrec<ST>(p.x, p.y, p.z, p.aux);
+            dl = pk2(minkowski<PC>(a, rawrec<ST>(lo2(q.x), lo2(q.y), lo2(q.z), lo2(q.aux)), kp),
+                     minkowski<PC>(a, rawrec<ST>(hi2(q.x), hi2(q.y), hi2(q.z), hi2(q.aux)), kp));
         }
     }
 }
@@ -794,7 +858,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     // neutral gray pixel; tiles inside the image skip the border resolution.
     float4 *tmp = reinterpret_cast<float4 *>(sD);
     static_assert((size_t)C::NPL * RN * sizeof(DT) >= (size_t)RN * sizeof(float4), "staging temp fits");
-    const float pad_aux = (ST == ST_MINIMAX) ? 0.57735026f : (ST == ST_CHROMA ? (1.f / 3.f) : 0.f);
+    const float pad_aux = (ST == ST_MINIMAX) ? 0.57735026f : (ST == ST_CHROMA ? (1.f / 3.f) : 1.7320508f);
     const int gy_top = kp.out_row0 + tile_y0 - H;  // global row of region row 0
     const bool inside = gy_top >= kp.in_row0 && gy_top + RH <= kp.in_row0 + kp.in_rows &&
                         gy_top >= 0 && gy_top + RH <= kp.global_H && tile_x0 - H >= 0 && tile_x0 - H + RW <= kp.W;
@@ -815,10 +879,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         const bool zero = (r8 | g8 | b8) == 0;
         any_zero |= zero;
         const float gx = zero ? 1.f : (float)r8, gy = zero ? 1.f : (float)g8, gz = zero ? 1.f : (float)b8;
-        float aux = 0.f;
-        if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(gz, gz, fmaf(gy, gy, gx * gx)));
-        if (ST == ST_CHROMA) aux = __frcp_rn(gx + gy + gz);
-        aux = __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
+        const float aux = encode_aux<ST, C::NEED_L>(gx, gy, gz, zero);
         sK[idx] = r8 | (g8 << 8) | (b8 << 16);
         tmp[idx] = make_float4(gx, gy, gz, aux);
     }
@@ -957,7 +1018,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         const int ry0 = ty * OPT + o;  // window top row in region coordinates
         const int oy = tile_y0 + ry0;
         const bool valid = (oy < kp.out_rows) && (ox < kp.W);
-        int b;
+        uint32_t kc;
         bool doubt;
         {
             auto col = [&](auto ic) {
@@ -969,15 +1030,15 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                 auto L = [&](auto ic) { return hi2(ag[o][decltype(ic)::value]); };
                 auto AD = [&](auto ic) { if constexpr (ACW) return lo2(cen[o][decltype(ic)::value]); else return 0.f; };
                 auto LD = [&](auto ic) { if constexpr (ACW) return hi2(cen[o][decltype(ic)::value]); else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, b, doubt);
+                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, kc, doubt);
             } else if constexpr (C::NEED_A) {
                 auto V = [&](auto ic) { return aA[o][decltype(ic)::value]; };
                 auto Z = [](auto) { return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, b, doubt);
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, kc, doubt);
             } else {
                 auto V = [&](auto ic) { return aL[o][decltype(ic)::value]; };
                 auto Z = [](auto) { return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, b, doubt);
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, kc, doubt);
             }
         }
 
@@ -996,7 +1057,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         }
 
         if (valid) {
-            const uint32_t col = sK[(ry0 + b / S) * RW + tx + b % S];
+            const uint32_t col = kc;
             uint8_t *op = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch + ox * 3;
             op[0] = (uint8_t)(col & 0xff);
             op[1] = (uint8_t)((col >> 8) & 0xff);
@@ -1097,8 +1158,9 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
         // warps) the CTA kernel's finer tiles win
         // (DFG_S3_KERNEL=cta|w3 forces one; read per call so tests can switch)
         const char *force = getenv("DFG_S3_KERNEL");
-        const long long strip_rows = (long long)((kp.W + 27) / 28) * kp.out_rows * kp.n_frames;
-        const bool w3 = force ? (force[0] == 'w') : (strip_rows >= 32768);
+        const long long strip_rows = (long long)((kp.W + 29) / 30) * kp.out_rows * kp.n_frames;
+        const bool w3 = kp.hostio || (kp.in_pitch <= 0xffffffffLL &&
+                                      (force ? (force[0] == 'w') : (kp.w3_rpc > 0 || strip_rows >= 32768)));
         if (w3) return launch_w3<FAM, ST, PC>(st, in, out, kp);
     }
     using SH = Shape<S, FAM>;

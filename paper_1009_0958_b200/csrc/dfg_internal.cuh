@@ -49,6 +49,11 @@ struct KParams {
     unsigned *flag_count;  // [0] pixels re-decided in float64, [1] of those needing pass 2
     // diagnostics: 2n floats per pixel (angular aggregates, Minkowski aggregates)
     float *dbg;
+    // 3x3 schedule hint: > 0 = the warp row-sweep kernel with this many rows
+    // per chunk (host pipeline bands: short latency, overlapping launches)
+    int w3_rpc;
+    // 1: in / out are mapped pinned host buffers (3x3 zero-copy host path)
+    int hostio;
 };
 
 // Border policy resolution (image.py:158-176): replicate = clamp,

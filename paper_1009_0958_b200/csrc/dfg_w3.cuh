@@ -2,7 +2,7 @@
 //
 // Same arithmetic, error budget and float64 re-decision as dfg_fast.cuh, with
 // a schedule built for the small window: every warp owns a strip of 32 input
-// columns (28 output columns, lanes 2..29) and sweeps DOWN a chunk of rows.
+// columns (30 output columns, lanes 1..30) and sweeps DOWN a chunk of rows.
 // Per row step each lane
 //   1. stages its new pixel into a warp-private 3-row ring of records,
 //   2. evaluates the 12 pairs whose LOWER pixel is that pixel
@@ -26,7 +26,11 @@ struct W3Cfg {
     static constexpr bool BOTH = NEED_A && NEED_L;
     using DT = typename std::conditional<BOTH, float2, float>::type;
     static constexpr int WARPS = 2;
-    static constexpr int LANES_E = 34;  // ring row width in elements (pads for pair loads at lane 31)
+    // ring row: element e = 2 + l holds the pixel pair (l, l+1); element 1 =
+    // (pad, pixel 0) serves lane 1's same-row partner, element 0 is the pad
+    // lane 0's (unused) same-row partner load touches
+    static constexpr int EOFF = 2;
+    static constexpr int LANES_E = 34;
     // per-warp shared layout (bytes)
     static constexpr int REC_BYTES = 3 * LANES_E * 32;         // 2 x float4 per element (A, B)
     static constexpr int COL_BYTES = 3 * 32 * 4;               // packed colours
@@ -35,7 +39,8 @@ struct W3Cfg {
     // du <= 1 entries of the previous row and du = 0 entries two rows up
     static constexpr int E_BYTES = (3 * 7 + 5) * 32 * (int)sizeof(DT);
     static constexpr int F64_BYTES = 9 * (int)sizeof(E64) + 2 * 36 * 8 + 16;
-    static constexpr int WARP_BYTES = (REC_BYTES + COL_BYTES + E_BYTES + F64_BYTES + 15) & ~15;
+    static constexpr int OUT_BYTES = 96;  // host-I/O output row staging (30 pixels)
+    static constexpr int WARP_BYTES = (REC_BYTES + COL_BYTES + E_BYTES + F64_BYTES + OUT_BYTES + 15) & ~15;
     static constexpr size_t kSmem = (size_t)WARPS * WARP_BYTES;
 };
 
@@ -43,10 +48,21 @@ struct W3Cfg {
 // du = 1 -> dv -2..2 (k 2..6); du = 2 -> dv -2..2 (k 7..11)
 __host__ __device__ constexpr int w3_k(int du, int dv) { return du == 0 ? dv - 1 : 2 + (du - 1) * 5 + (dv + 2); }
 
-template <int FAM, int ST, int PC>
-__global__ void __launch_bounds__(64, 9)
-dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const KParams kp, int rows_per_chunk,
-              int n_strips, int n_chunks)
+// resident blocks per SM: 9 (18 warps, 96 registers); the minimax route's
+// two polynomials need more registers -> 8 (16 warps, 128 registers)
+template <int ST>
+constexpr int w3_minb() { return ST == ST_MINIMAX ? 8 : 9; }
+
+// HIO (host I/O): `in` / `out` are mapped pinned HOST buffers -- the kernel
+// streams its rows over PCIe itself (the host path's zero-copy mode): each
+// warp row is read as aligned 32-bit words (<= 25 per 32-pixel strip row,
+// bytes redistributed by shuffles) and written as aligned words assembled in
+// shared memory, so PCIe sees full coalesced requests in both directions
+// (full duplex) while the SMs compute.
+template <int FAM, int ST, int PC, bool HIO>
+__global__ void __launch_bounds__(64, w3_minb<ST>())
+dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const KParams kp, int n_strips,
+              int n_chunks)
 {
     using C = W3Cfg<FAM>;
     using DT = typename C::DT;
@@ -69,57 +85,108 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
     DT *rE = reinterpret_cast<DT *>(wb + C::REC_BYTES + C::COL_BYTES);  // [3][7][32] + [5][32]
     DT *rE2 = rE + 3 * 7 * 32;
     unsigned char *f64b = wb + C::REC_BYTES + C::COL_BYTES + C::E_BYTES;
+    uint8_t *ostage = f64b + C::F64_BYTES;  // HIO output row staging
 
-    const int col = strip * 28 - 2 + lane;  // input column of this lane
+    const int col = strip * 30 - 1 + lane;  // input column of this lane
     const int colr = resolve_idx(col, kp.W, kp.border);
-    const int oy0 = chunk * rows_per_chunk;  // first output row (strip-local) of the chunk
-    const int oy1 = min(kp.out_rows, oy0 + rows_per_chunk);
+    // output rows [oy0, oy1) of the chunk (strip-local)
+    const int oy0 = (int)((long long)chunk * kp.out_rows / n_chunks);
+    const int oy1 = (int)((long long)(chunk + 1) * kp.out_rows / n_chunks);
 
-    // pad elements (lanes 32, 33) of every ring row: neutral, never used
-    if (lane < 2) {
-        for (int r = 0; r < 3; r++) {
-            rA[r * C::LANES_E + 32 + lane] = make_float4(1.f, 1.f, 1.f, 1.f);
-            rB[r * C::LANES_E + 32 + lane] = make_float4(1.f, 1.f, 1.f, 1.f);
-        }
+    // pad element 0 of every ring row: neutral, never used
+    if (lane < 3) {
+        rA[lane * C::LANES_E] = make_float4(1.f, 1.f, 1.f, 1.f);
+        rB[lane * C::LANES_E] = make_float4(1.f, 1.f, 1.f, 1.f);
     }
 
     bool zr0 = false, zr1 = false;  // zero vectors in the two previous staged rows
     // the pixel of the next row step is loaded one step ahead (its HBM
     // latency hides behind the current step's pair math)
+    const uint8_t *cbase = fin + colr * 3;
+    const unsigned pitch = (unsigned)kp.in_pitch;  // the host keeps rows < 4 GiB
+    auto row_of = [&](int yy) {
+        int gy = kp.out_row0 + yy;
+        if ((unsigned)gy >= (unsigned)kp.global_H) gy = resolve_idx(gy, kp.global_H, kp.border);
+        return min(max(gy - kp.in_row0, 0), kp.in_rows - 1);
+    };
     auto load_px = [&](int yy, uint32_t &r, uint32_t &g, uint32_t &b) {
-        int gy = resolve_idx(kp.out_row0 + yy, kp.global_H, kp.border) - kp.in_row0;
-        gy = min(max(gy, 0), kp.in_rows - 1);
-        const uint8_t *px = fin + (long long)gy * kp.in_pitch + colr * 3;
+        const uint8_t *px = cbase + (size_t)((unsigned long long)(unsigned)row_of(yy) * pitch);
         r = px[0];
         g = px[1];
         b = px[2];
     };
-    uint32_t nr8, ng8, nb8;
-    load_px(oy0 - 1, nr8, ng8, nb8);
+    // HIO: in-range columns [c_lo, c_hi) of this strip arrive as the aligned
+    // words covering their bytes (an aligned word never crosses a page, so
+    // the over-read at either end is harmless); out-of-range (border) lanes
+    // load their resolved column's bytes directly
+    const int c_lo = max(strip * 30 - 1, 0), c_hi = min(strip * 30 + 31, kp.W);
+    const bool in_range = col >= 0 && col < kp.W;
+    struct Pend {
+        uint32_t word, r, g, b;
+        int mis;  // byte offset of column c_lo within its aligned word
+    };
+    auto load_hio = [&](int yy, Pend &pd) {
+        const uint8_t *rowp = fin + (size_t)((unsigned long long)(unsigned)row_of(yy) * pitch);
+        const uintptr_t lo = (uintptr_t)(rowp + 3 * c_lo), hi = (uintptr_t)(rowp + 3 * c_hi);
+        const uintptr_t wa = (lo & ~(uintptr_t)3) + 4 * (uintptr_t)lane;
+        pd.mis = (int)(lo & 3);
+        pd.word = wa < hi ? *reinterpret_cast<const uint32_t *>(wa) : 0u;
+        if (!in_range) {
+            const uint8_t *px = rowp + colr * 3;
+            pd.r = px[0];
+            pd.g = px[1];
+            pd.b = px[2];
+        }
+    };
+    auto unpack_hio = [&](const Pend &pd, uint32_t &r, uint32_t &g, uint32_t &b) {
+        const int off = 3 * (max(col, 0) - c_lo) + pd.mis;
+        const uint32_t w0 = __shfl_sync(0xffffffffu, pd.word, (off >> 2) & 31);
+        const uint32_t w1 = __shfl_sync(0xffffffffu, pd.word, ((off >> 2) + 1) & 31);
+        const uint32_t v = __funnelshift_r(w0, w1, 8 * (off & 3));
+        r = in_range ? (v & 0xffu) : pd.r;
+        g = in_range ? ((v >> 8) & 0xffu) : pd.g;
+        b = in_range ? ((v >> 16) & 0xffu) : pd.b;
+    };
+    uint32_t nr8 = 0, ng8 = 0, nb8 = 0;
+    Pend pend{};
+    if constexpr (HIO) load_hio(oy0 - 1, pend);
+    else load_px(oy0 - 1, nr8, ng8, nb8);
+    // this lane's pixels of the previous two row steps (the vertical pair's
+    // partners for lane l-2); neutral until the warm-up steps fill them
+    Pix pm1 = {1.f, 1.f, 1.f, 1.f}, pm2 = {1.f, 1.f, 1.f, 1.f};
     // row step y (strip-local input row, window of output row y - 1)
     for (int y = oy0 - 1; y <= oy1; y++) {
         const int slot = (y + 3) % 3;
         __syncwarp();  // the previous step's readers are done with this slot
         // ---- 1. stage the new pixel ---------------------------------------
-        const uint32_t r8 = nr8, g8 = ng8, b8 = nb8;
-        if (y < oy1) load_px(y + 1, nr8, ng8, nb8);
+        uint32_t r8, g8, b8;
+        if constexpr (HIO) {
+            unpack_hio(pend, r8, g8, b8);
+            if (y < oy1) load_hio(y + 1, pend);
+        } else {
+            r8 = nr8;
+            g8 = ng8;
+            b8 = nb8;
+            if (y < oy1) load_px(y + 1, nr8, ng8, nb8);
+        }
         const bool zero = (r8 | g8 | b8) == 0;
         Pix q;
         // exact u8 -> float without I2F: 2^23 + v, minus 2^23
         q.x = zero ? 1.f : __uint_as_float(0x4B000000u | r8) - 8388608.f;
         q.y = zero ? 1.f : __uint_as_float(0x4B000000u | g8) - 8388608.f;
         q.z = zero ? 1.f : __uint_as_float(0x4B000000u | b8) - 8388608.f;
-        float aux = 0.f;
-        if (ST == ST_MINIMAX) aux = rsqrtf(fmaf(q.z, q.z, fmaf(q.y, q.y, q.x * q.x)));
-        if (ST == ST_CHROMA) aux = __frcp_rn(q.x + q.y + q.z);
-        q.aux = __uint_as_float((__float_as_uint(aux) & ~1u) | (zero ? 1u : 0u));
+        q.aux = encode_aux<ST, C::NEED_L>(q.x, q.y, q.z, zero);
         {
             // element l = pixel pair (l, l+1): the right neighbour's record by
             // shuffle, two whole 16-byte stores (lane 31's second half: unused)
             const float sx = __shfl_down_sync(0xffffffffu, q.x, 1), sy = __shfl_down_sync(0xffffffffu, q.y, 1);
             const float sz = __shfl_down_sync(0xffffffffu, q.z, 1), sa = __shfl_down_sync(0xffffffffu, q.aux, 1);
-            rA[slot * C::LANES_E + lane] = make_float4(q.x, sx, q.y, sy);
-            rB[slot * C::LANES_E + lane] = make_float4(q.z, sz, q.aux, sa);
+            rA[slot * C::LANES_E + C::EOFF + lane] = make_float4(q.x, sx, q.y, sy);
+            rB[slot * C::LANES_E + C::EOFF + lane] = make_float4(q.z, sz, q.aux, sa);
+            if (lane == 0) {  // element 1 = (pad, pixel 0)
+                rA[slot * C::LANES_E + 1] = make_float4(1.f, q.x, 1.f, q.y);
+                rB[slot * C::LANES_E + 1] = make_float4(1.f, q.z, 1.f, q.aux);
+            }
             rK[slot * 32 + lane] = r8 | (g8 << 8) | (b8 << 16);
         }
         const bool zr2 = __any_sync(0xffffffffu, zero);
@@ -128,8 +195,15 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         zr1 = zr2;
         __syncwarp();
         // ---- 2. pair values with lower pixel q ------------------------------
-        // partner pairs (p, p+1) as packed elements: row y: lanes (l-2, l-1);
-        // rows y-1, y-2: lanes (l-2,l-1), (l,l+1), (l+2, l+3: dummy)
+        // six packed evaluations for the 12 partners: row y: element
+        // (l-2, l-1); rows y-1 and y-2: elements (l-2, l-1), (l, l+1); and
+        // the vertical pair {(y-1, l+2), (y-2, l+2)}, shuffled in from lane
+        // l+2's own previous two pixels (no shared-memory round trip)
+        Pair2 pv;
+        pv.x = pk2(__shfl_down_sync(0xffffffffu, pm1.x, 2), __shfl_down_sync(0xffffffffu, pm2.x, 2));
+        pv.y = pk2(__shfl_down_sync(0xffffffffu, pm1.y, 2), __shfl_down_sync(0xffffffffu, pm2.y, 2));
+        pv.z = pk2(__shfl_down_sync(0xffffffffu, pm1.z, 2), __shfl_down_sync(0xffffffffu, pm2.z, 2));
+        pv.aux = pk2(__shfl_down_sync(0xffffffffu, pm1.aux, 2), __shfl_down_sync(0xffffffffu, pm2.aux, 2));
         auto eval = [&](auto zc_c) {
             constexpr bool ZC = decltype(zc_c)::value;
             auto put = [&](int k, float a, float l) {
@@ -140,42 +214,45 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                 if (k < 7) rE[(slot * 7 + k) * 32 + lane] = v;
                 else rE2[(k - 7) * 32 + lane] = v;
             };
-            const int el_m2 = max(lane - 2, 0);  // lanes 0, 1: partners outside the strip (values unused)
-            // all partner loads first, then the seven independent packed pair
+            // all partner loads first, then the six independent packed pair
             // evaluations, then the stores: the pair math chains interleave
             const int rs1 = (y + 2) % 3, rs2 = (y + 1) % 3;
-            const int rsl[7] = {slot, rs1, rs1, rs1, rs2, rs2, rs2};
-            const int els[7] = {el_m2, el_m2, lane, lane + 2, el_m2, lane, lane + 2};
-            Pair2 pp[7];
+            const int rsl[5] = {slot, rs1, rs1, rs2, rs2};
+            const int els[5] = {lane, lane, lane + 2, lane, lane + 2};  // lane 0's (l-2, l-1): pads, unused
+            Pair2 pp[6];
 #pragma unroll
-            for (int t = 0; t < 7; t++) {
+            for (int t = 0; t < 5; t++) {
                 const ulonglong2 A2 = lds_u2(rA + rsl[t] * C::LANES_E + els[t]);
                 const ulonglong2 B2 = lds_u2(rB + rsl[t] * C::LANES_E + els[t]);
                 pp[t] = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
             }
-            P2 da[7], dl[7];
+            pp[5] = pv;
+            P2 da[6], dl[6];
 #pragma unroll
-            for (int t = 0; t < 7; t++) pair_values2<FAM, ST, PC, ZC>(q, pp[t], kp, da[t], dl[t]);
+            for (int t = 0; t < 6; t++) pair_values2<FAM, ST, PC, ZC>(q, pp[t], kp, da[t], dl[t]);
             // du = 0: partners (l-2, l-1) = dv 2, 1
             put(w3_k(0, 2), lo2(da[0]), lo2(dl[0]));
             put(w3_k(0, 1), hi2(da[0]), hi2(dl[0]));
 #pragma unroll
             for (int du = 1; du <= 2; du++) {
-                const int t = 1 + 3 * (du - 1);
+                const int t = 1 + 2 * (du - 1);
                 put(w3_k(du, 2), lo2(da[t]), lo2(dl[t]));  // partners l-2, l-1 -> dv = 2, 1
                 put(w3_k(du, 1), hi2(da[t]), hi2(dl[t]));
                 put(w3_k(du, 0), lo2(da[t + 1]), lo2(dl[t + 1]));  // partners l, l+1 -> dv = 0, -1
                 put(w3_k(du, -1), hi2(da[t + 1]), hi2(dl[t + 1]));
-                put(w3_k(du, -2), lo2(da[t + 2]), lo2(dl[t + 2]));  // partner l+2 -> dv = -2
             }
+            put(w3_k(1, -2), lo2(da[5]), lo2(dl[5]));  // vertical pair: partner l+2 in rows y-1, y-2
+            put(w3_k(2, -2), hi2(da[5]), hi2(dl[5]));
         };
         if (zchk) eval(std::true_type{});
         else eval(std::false_type{});
+        pm2 = pm1;
+        pm1 = q;
         __syncwarp();
         // ---- 3. aggregate + select for output row y - 1 ---------------------
         const int oy = y - 1;
         if (oy < oy0) continue;  // warm-up rows (uniform across the warp)
-        const bool valid = lane >= 2 && lane < 30 && oy < oy1 && col < kp.W;
+        const bool valid = lane >= 1 && lane < 31 && oy < oy1 && col < kp.W;
         P2 ag[BOTH ? N : 1], cen[ACW ? N : 1];
         float aS[BOTH ? 1 : N];
 #pragma unroll
@@ -216,7 +293,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         uint32_t wc[N];
 #pragma unroll
         for (int i = 0; i < N; i++) wc[i] = kR[i / 3][i % 3];
-        int b;
+        uint32_t cb;
         bool doubt;
         {
             auto col = [&](auto ic) { return wc[decltype(ic)::value]; };
@@ -225,11 +302,11 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                 auto L = [&](auto ic) { return hi2(ag[decltype(ic)::value]); };
                 auto AD = [&](auto ic) { if constexpr (ACW) return lo2(cen[decltype(ic)::value]); else return 0.f; };
                 auto LD = [&](auto ic) { if constexpr (ACW) return hi2(cen[decltype(ic)::value]); else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, b, doubt);
+                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, cb, doubt);
             } else {
                 auto V = [&](auto ic) { return aS[decltype(ic)::value]; };
                 auto Z = [](auto) { return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, b, doubt);
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, cb, doubt);
             }
         }
         uint8_t *orow = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch;
@@ -247,10 +324,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
             }
         }
         if (valid) {
-            uint32_t cb = wc[0];
-#pragma unroll
-            for (int i = 1; i < N; i++) cb = (b == i) ? wc[i] : cb;
-            uint8_t *op = orow + col * 3;
+            uint8_t *op = HIO ? ostage + 3 * (lane - 1) : orow + col * 3;
             op[0] = (uint8_t)(cb & 0xff);
             op[1] = (uint8_t)((cb >> 8) & 0xff);
             op[2] = (uint8_t)((cb >> 16) & 0xff);
@@ -284,12 +358,33 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                     bb = decide64(e64, kp.fp, lane, dA, dL, &m);
                 }
                 if (lane == 0) {
-                    uint8_t *op = orow + (strip * 28 - 2 + fl) * 3;
+                    uint8_t *op = HIO ? ostage + 3 * (fl - 1) : orow + (strip * 30 - 1 + fl) * 3;
                     op[0] = (uint8_t)e64[bb].raw[0];
                     op[1] = (uint8_t)e64[bb].raw[1];
                     op[2] = (uint8_t)e64[bb].raw[2];
                 }
                 __syncwarp();
+            }
+        }
+        if constexpr (HIO) {  // the staged row segment -> host as aligned words
+            __syncwarp();
+            const int nv = min(30, kp.W - strip * 30);
+            if (oy < oy1 && nv > 0) {
+                const uintptr_t A = (uintptr_t)(orow + 3 * (strip * 30)), E = A + 3 * (uintptr_t)nv;
+                const uintptr_t wa = (A & ~(uintptr_t)3) + 4 * (uintptr_t)lane;
+                if (wa < E) {
+                    if (wa >= A && wa + 4 <= E) {
+                        const int o = (int)(wa - A);
+                        *reinterpret_cast<uint32_t *>(wa) = (uint32_t)ostage[o] | ((uint32_t)ostage[o + 1] << 8) |
+                                                            ((uint32_t)ostage[o + 2] << 16) |
+                                                            ((uint32_t)ostage[o + 3] << 24);
+                    } else {
+                        for (int k = 0; k < 4; k++) {
+                            const uintptr_t a = wa + k;
+                            if (a >= A && a < E) *reinterpret_cast<uint8_t *>(a) = ostage[a - A];
+                        }
+                    }
+                }
             }
         }
     }
@@ -299,30 +394,40 @@ template <int FAM, int ST, int PC>
 cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp)
 {
     using C = W3Cfg<FAM>;
-    auto kern = dfg_w3_kernel<FAM, ST, PC>;
-    static unsigned long long configured = 0;
+    auto kern = kp.hostio ? dfg_w3_kernel<FAM, ST, PC, true> : dfg_w3_kernel<FAM, ST, PC, false>;
+    static unsigned long long configured[2] = {0, 0};
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!(configured & (1ull << (dev & 63)))) {
+    if (!(configured[kp.hostio] & (1ull << (dev & 63)))) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
         if (e != cudaSuccess) return e;
-        configured |= 1ull << (dev & 63);
+        configured[kp.hostio] |= 1ull << (dev & 63);
     }
-    const int n_strips = (kp.W + 27) / 28;
-    // rows per chunk: about one wave of resident warps (16 per SM), more
-    // rows (fewer warm-up rows, 2 per chunk) when the input is taller
-    const long long strip_rows = (long long)n_strips * kp.out_rows * kp.n_frames;
+    const int n_strips = (kp.W + 29) / 30;
+    // chunks per strip: fill whole waves of resident warps (WPS per SM) with
+    // equal row counts (chunk c covers rows [c R / n, (c+1) R / n)), at most
+    // 64 rows per chunk; every chunk pays 2 warm-up row steps
+    static const int env_wps = [] {
+        const char *e = getenv("DFG_W3_WPS");  // diagnostics only
+        return e ? atoi(e) : 0;
+    }();
     static const int rpc_env = [] {
         const char *e = getenv("DFG_W3_RPC");  // diagnostics only
         return e ? atoi(e) : 0;
     }();
-    int rpc = (int)(strip_rows / (148 * 16));
-    rpc = rpc < 16 ? 16 : (rpc > 64 ? 64 : rpc);
-    if (rpc_env > 0) rpc = rpc_env;
-    const int n_chunks = (kp.out_rows + rpc - 1) / rpc;
-    const int warps = n_strips * n_chunks;
+    const long long wps = env_wps > 0 ? env_wps : 16;
+    const long long slots = 148 * wps;
+    const long long cols = (long long)n_strips * kp.n_frames;  // independent strip columns
+    const long long strip_rows = cols * kp.out_rows;
+    const long long waves = (strip_rows + slots * 64 - 1) / (slots * 64);
+    long long n_chunks = (waves * slots) / cols;
+    const int rpc_hint = rpc_env > 0 ? rpc_env : kp.w3_rpc;  // host pipeline bands: short chunks
+    if (rpc_hint > 0) n_chunks = (kp.out_rows + rpc_hint - 1) / rpc_hint;
+    n_chunks = n_chunks < 1 ? 1 : (n_chunks > kp.out_rows ? kp.out_rows : n_chunks);
+    n_chunks = n_chunks < (kp.out_rows + 63) / 64 ? (kp.out_rows + 63) / 64 : n_chunks;
+    const int warps = n_strips * (int)n_chunks;
     dim3 grid((warps + C::WARPS - 1) / C::WARPS, 1, kp.n_frames);
-    kern<<<grid, C::WARPS * 32, C::kSmem, st>>>(in, out, kp, rpc, n_strips, n_chunks);
+    kern<<<grid, C::WARPS * 32, C::kSmem, st>>>(in, out, kp, n_strips, (int)n_chunks);
     return cudaGetLastError();
 }
 

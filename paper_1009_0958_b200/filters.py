@@ -55,6 +55,7 @@ def _params(spec, policy):
         key = (spec, mode)
         prm = _prm_cache.get(key)
     except TypeError:  # unhashable duck-typed spec
+        _validate_spec(spec)
         return _lib.params_from_spec(spec, policy)
     if prm is None:
         _validate_spec(spec)
@@ -112,8 +113,10 @@ def workspace(nbytes: int, device=None):
 
 
 def _stream_ptr(torch, stream, device):
-    s = stream if stream is not None else torch.cuda.current_stream(device)
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
+    idx = torch.cuda.current_device() if device is None else torch.device(device).index
+    return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(idx))  # no Stream object per call
 
 
 def filter_device(x, spec, policy=REPLICATE, out=None, stream=None, ws=None):
@@ -194,12 +197,16 @@ def filter_host(pixels_u8: np.ndarray, spec, policy=REPLICATE, out: np.ndarray |
     """The C ABI's host-buffer path (``dfg_filter_host``): host uint8 in,
     host uint8 out, H2D + kernels + D2H inside one call."""
     torch = _torch()
-    _validate_spec(spec)
-    a = np.ascontiguousarray(pixels_u8, dtype=np.uint8)
+    prm = _params(spec, policy)  # validates on first use of a spec
+    a = pixels_u8 if (type(pixels_u8) is np.ndarray and pixels_u8.dtype == np.uint8 and
+                      pixels_u8.flags.c_contiguous) else np.ascontiguousarray(pixels_u8, dtype=np.uint8)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise ValueError(f"pixel array must have shape (M, N, 3), got {a.shape}")
     H, W = a.shape[:2]
     if out is None:
         out = np.empty_like(a)
-    prm = _params(spec, policy)
+    elif out.shape != a.shape or out.dtype != np.uint8 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous uint8 array of the input's shape")
     rc = _lib.lib().dfg_filter_host(a.ctypes.data_as(ctypes.c_void_p), H, W,
                                     out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(prm),
                                     _stream_ptr(torch, stream, None))

@@ -207,3 +207,33 @@ def test_3x3_kernels_against_oracle(cuda, spec, kernel, monkeypatch):
     x = torch.from_numpy(img).cuda()
     got = filter_rows_device(x[30:91], 120, 30, 31, 59, s).cpu().numpy()
     assert (got == full[31:90]).all()
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("spec", ["ddf:exact", "bvdf:minimax:q=3", "acwddf:rgb", "vmf", "ddf:exact:p=1"])
+def test_host_streaming_3x3_against_oracle(cuda, spec, mode, monkeypatch):
+    """3x3 with pinned host buffers, banded copies (mode 0) and the opt-in
+    zero-copy streaming modes (1: the kernel reads and writes the mapped
+    host memory itself as aligned words; 2: input only; 3: output only).
+    Odd byte offsets of the buffers, widths whose rows are not 4-byte
+    multiples, single-row / single-column images, both borders and zero
+    vectors must all reproduce the oracle bit for bit."""
+    torch = cuda
+    monkeypatch.setenv("DFG_HOST_STREAM", mode)
+    s = parse_filter_spec(spec)
+    for H, W, seed, border, shift in ((97, 61, 3, "replicate", 0), (40, 29, 4, "reflect", 1), (133, 90, 5, "replicate", 3),
+                                      (1, 37, 6, "replicate", 2), (23, 1, 7, "reflect", 1), (64, 31, 8, "reflect", 0)):
+        img = synth.noisy_image(H, W, seed, ("correlated", 0.2))
+        if H > 9 and W > 12:
+            img[5:9, 7:12] = 0
+        n = img.size
+        buf_in = torch.zeros(n + 8, dtype=torch.uint8).pin_memory()
+        buf_out = torch.full((n + 8,), 7, dtype=torch.uint8).pin_memory()
+        a_in = buf_in.numpy()[shift:shift + n].reshape(img.shape)
+        a_out = buf_out.numpy()[3 - shift:3 - shift + n].reshape(img.shape)
+        a_in[...] = img
+        got = filter_host(a_in, s, _policy(border), out=a_out)
+        want = oracle.filter_image(img, s, border)
+        assert (got == want).all(), (spec, H, W, border, int((got != want).any(-1).sum()))
+        guard = buf_out.numpy()
+        assert (guard[:3 - shift] == 7).all() and (guard[3 - shift + n:] == 7).all()  # no stray writes
