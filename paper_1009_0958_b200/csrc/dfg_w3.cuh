@@ -48,10 +48,11 @@ struct W3Cfg {
 // du = 1 -> dv -2..2 (k 2..6); du = 2 -> dv -2..2 (k 7..11)
 __host__ __device__ constexpr int w3_k(int du, int dv) { return du == 0 ? dv - 1 : 2 + (du - 1) * 5 + (dv + 2); }
 
-// resident blocks per SM: 9 (18 warps, 96 registers); the minimax route's
-// two polynomials need more registers -> 8 (16 warps, 128 registers)
+// resident blocks per SM: 9 (18 warps, 96 registers) for the exact route;
+// the minimax route's two polynomials and the chromaticity route's sums
+// need more registers -> 8 (16 warps, 128 registers)
 template <int ST>
-constexpr int w3_minb() { return ST == ST_MINIMAX ? 8 : 9; }
+constexpr int w3_minb() { return ST == ST_EXACT ? 9 : 8; }
 
 // HIO (host I/O): `in` / `out` are mapped pinned HOST buffers -- the kernel
 // streams its rows over PCIe itself (the host path's zero-copy mode): each
@@ -154,9 +155,17 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
     // this lane's pixels of the previous two row steps (the vertical pair's
     // partners for lane l-2); neutral until the warm-up steps fill them
     Pix pm1 = {1.f, 1.f, 1.f, 1.f}, pm2 = {1.f, 1.f, 1.f, 1.f};
+    // ring slots of rows y, y-1, y-2 (rotated each step, no modulo)
+    int sl0 = 0, sl1 = 2, sl2 = 1;
+    auto rotate = [&] {
+        const int t = sl2;
+        sl2 = sl1;
+        sl1 = sl0;
+        sl0 = t;
+    };
     // row step y (strip-local input row, window of output row y - 1)
-    for (int y = oy0 - 1; y <= oy1; y++) {
-        const int slot = (y + 3) % 3;
+    for (int y = oy0 - 1; y <= oy1; y++, rotate()) {
+        const int slot = sl0;
         __syncwarp();  // the previous step's readers are done with this slot
         // ---- 1. stage the new pixel ---------------------------------------
         uint32_t r8, g8, b8;
@@ -216,7 +225,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
             };
             // all partner loads first, then the six independent packed pair
             // evaluations, then the stores: the pair math chains interleave
-            const int rs1 = (y + 2) % 3, rs2 = (y + 1) % 3;
+            const int rs1 = sl1, rs2 = sl2;
             const int rsl[5] = {slot, rs1, rs1, rs2, rs2};
             const int els[5] = {lane, lane, lane + 2, lane, lane + 2};  // lane 0's (l-2, l-1): pads, unused
             Pair2 pp[6];
@@ -263,7 +272,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         if constexpr (ACW) cen[DC] = pk2(kp.self_term, 0.f);
         const int lc = min(max(lane, 1), 30);  // clamp so lanes 0/31 read in-bounds (results unused)
         // ring rows of the window's input rows oy-1, oy, oy+1 (slots of y-2, y-1, y)
-        const int s0 = (oy + 2) % 3, s1 = (oy + 3) % 3, s2 = slot;
+        const int s0 = sl2, s1 = sl1, s2 = sl0;
         const DT *eR[3] = {rE + s0 * 7 * 32 + lc - 1, rE + s1 * 7 * 32 + lc - 1, rE + s2 * 7 * 32 + lc - 1};
         const DT *eR2 = rE2 + lc - 1;
         const uint32_t *kR[3] = {rK + s0 * 32 + lc - 1, rK + s1 * 32 + lc - 1, rK + s2 * 32 + lc - 1};
@@ -341,7 +350,8 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                 mask &= mask - 1;
                 if (lane < N) {
                     const int i = lane;
-                    const uint32_t cc = rK[((oy - 1 + i / 3 + 3) % 3) * 32 + fl - 1 + i % 3];
+                    const int sr = i < 3 ? sl2 : (i < 6 ? sl1 : sl0);
+                    const uint32_t cc = rK[sr * 32 + fl - 1 + i % 3];
                     prep64(make_float4((float)(cc & 0xff), (float)((cc >> 8) & 0xff), (float)((cc >> 16) & 0xff), 0.f),
                            ST, e64[i]);
                 }
