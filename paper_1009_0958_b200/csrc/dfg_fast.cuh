@@ -1021,9 +1021,20 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         uint32_t kc;
         bool doubt;
         {
+            // window colours: up to 5x5 loaded once into registers for the
+            // selection's passes (every pick reads each candidate's colour
+            // twice); 7x7 reads them from shared memory (49 more registers
+            // would spill the aggregates)
+            constexpr bool WCR = N <= 25;
+            uint32_t wc[WCR ? N : 1];
+            if constexpr (WCR) {
+#pragma unroll
+                for (int i = 0; i < N; i++) wc[i] = sK[(ry0 + i / S) * RW + tx + i % S];
+            }
             auto col = [&](auto ic) {
                 constexpr int i = decltype(ic)::value;
-                return sK[(ry0 + i / S) * RW + tx + i % S];
+                if constexpr (WCR) return wc[i];
+                else return sK[(ry0 + i / S) * RW + tx + i % S];
             };
             if constexpr (BOTH) {
                 auto A = [&](auto ic) { return lo2(ag[o][decltype(ic)::value]); };
