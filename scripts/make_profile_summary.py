@@ -11,8 +11,9 @@ tag, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
 out = [f"# ncu summaries, round {tag}", "",
        "Captured on one B200 (sm_100a, driver 580.159) through `gpurun` with "
        "`ncu --set full --clock-control none --import-source on -k regex:dfg_ -s 3 -c 1` on "
-       "`python bench.py --config <c> --steps 1 --warmup 3 --no-cpu` (the first timed launch, after warm-up), "
-       "and the launch list with `--metrics gpu__time_duration.sum,... -c 40` on the default bench command. "
+       "`python bench.py --config <c> --steps 1 --warmup 3 --no-cpu` (the 4th launch: after the 3 warm-up steps), "
+       "and the launch list with `--metrics gpu__time_duration.sum,... --clock-control none -c 400` on the default "
+       "bench command (`scripts/gpu_profiles.sh`). "
        "Durations under ncu are cold-cache and serialised; the bench numbers come from CUDA events without ncu.", ""]
 
 # launch list shares
@@ -51,6 +52,7 @@ KEYS = [("gpu__time_duration.sum", "duration"), ("smsp__inst_executed.sum", "war
         ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "shared wavefronts"),
         ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "shared bank-conflict wavefronts"),
         ("dram__bytes_read.sum", "DRAM read"), ("dram__bytes_write.sum", "DRAM write")]
+traffic = {}
 for rep in reps:
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     r = list(csv.reader(io.StringIO(txt)))
@@ -67,5 +69,18 @@ for rep in reps:
     out.append("| top stall reasons (warps per issue) | " +
                ", ".join(f"{n.split('stalled_')[1].split('_per')[0]} {v:.2f}" for v, n in stalls) + " |")
     out.append("")
+    try:
+        def num(k):
+            v, u = d[k]
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3,
+                     "nsecond": 1e-9, "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1}.get(u.strip(), 1)
+            return float(v.replace(",", "")) * scale
+        traffic[Path(rep).stem.replace("prof_", "")] = {
+            "kernel": name, "dram_bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
+            "duration_s": num("gpu__time_duration.sum")}
+    except (KeyError, ValueError):
+        pass
 Path(f"profiles/{tag}_summary.md").write_text("\n".join(out) + "\n")
-print(f"profiles/{tag}_summary.md")
+import json  # noqa: E402
+Path(f"profiles/{tag}_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+print(f"profiles/{tag}_summary.md", f"profiles/{tag}_traffic.json")
