@@ -1165,13 +1165,14 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
     if constexpr (S == 3) {
         // 3x3: the warp-synchronous row-sweep kernel (dfg_w3.cuh); the CTA
         // kernel stays selectable for comparison (DFG_S3_CTA=1)
-        // for small inputs (too few strip-rows to fill the SMs with sweeping
-        // warps) the CTA kernel's finer tiles win
+        // for very small inputs (< 8 K strip-rows, e.g. 256^2) the CTA
+        // kernel's finer tiles win; from C1's 512^2 (9 K strip-rows, 28 vs
+        // 35 us on the config image) the row sweep does
         // (DFG_S3_KERNEL=cta|w3 forces one; read per call so tests can switch)
         const char *force = getenv("DFG_S3_KERNEL");
         const long long strip_rows = (long long)((kp.W + 29) / 30) * kp.out_rows * kp.n_frames;
         const bool w3 = kp.hostio || (kp.in_pitch <= 0xffffffffLL &&
-                                      (force ? (force[0] == 'w') : (kp.w3_rpc > 0 || strip_rows >= 32768)));
+                                      (force ? (force[0] == 'w') : (kp.w3_rpc > 0 || strip_rows >= 8192)));
         if (w3) return launch_w3<FAM, ST, PC>(st, in, out, kp);
     }
     using SH = Shape<S, FAM>;
