@@ -10,6 +10,9 @@
  *   _engine.run_rows(.., r0, r1)    _engine.py:560-583   dfg_filter_rows (row band)
  *   apply_filter(workers=k) bands   filters.py:416-430   dfg_filter_rows per GPU strip
  *   (frame loop in bench/CLI)       bench.py:96-109      dfg_filter_batch
+ *   noise.corrupt_image             noise.py:85-116      dfg_corrupt_image
+ *   metrics.compare / mae/psnr/ncd  metrics.py:64-118    dfg_image_metrics
+ *   calibration.fit_angular_...     calibration.py:83-125 dfg_calib_reduce/_samples
  *
  * The reference has no FFI of its own (pure Python + numba); these entry
  * points are what its filters.py would bind through ctypes -- INTEGRATION.md
@@ -120,8 +123,10 @@ DFG_API int dfg_filter_batch(const uint8_t *d_in, int32_t B, int32_t H, int32_t 
                      void *stream);
 
 /* End to end from HOST memory (pinned or pageable), synchronised before
- * return: cached per-thread device buffers and a row-band H2D / kernel /
- * D2H pipeline on `stream` and two copy streams (pinned buffers overlap). */
+ * return: cached per-thread device buffers and a row-band pipeline -- H2D
+ * and D2H copy streams, band kernels on four streams, each band's copy
+ * carrying its halo rows; with pinned buffers the pipeline is captured once
+ * and replayed as a CUDA graph (cache keyed on buffers, shape, params). */
 DFG_API int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out,
                     const dfg_params *prm, void *stream);
 
@@ -166,6 +171,26 @@ DFG_API int dfg_corrupt_image(const uint8_t *d_in, int32_t H, int32_t W, int64_t
 DFG_API int dfg_image_metrics(const uint8_t *d_ref, const uint8_t *d_test, int32_t H, int32_t W,
                       int64_t ref_pitch, int64_t test_pitch, double *out3, void *d_scratch,
                       void *stream);
+
+/* Angle-vs-chromaticity calibration sampling (reference calibration.py:83-125):
+ * `pairs` random RGB pairs drawn exactly as sample_angle_chromaticity_pairs
+ * draws them from np.random.PCG64(seed) (state/inc as for dfg_noise_params),
+ * B = chromaticity L_p distance, A = exact angle, float64.
+ * dfg_calib_reduce: mode 0 -> out3 = {sum B, sum A, 0}; mode 1 -> central
+ * second moments {sum (B-x0)^2, sum (A-x1)^2, sum (B-x0)(A-x1)}; mode 2 ->
+ * residuals about A = x0*B + x1: {sum r^2, sum |r|, 0}.  Deterministic
+ * (fixed-order reduction); synchronises `stream`.  d_scratch: device memory
+ * of dfg_calib_scratch_bytes().  dfg_calib_samples writes the samples. */
+typedef struct dfg_calib_params {
+    int64_t pairs;
+    double p;
+    uint64_t state_hi, state_lo, inc_hi, inc_lo;
+} dfg_calib_params;
+
+DFG_API size_t dfg_calib_scratch_bytes(void);
+DFG_API int dfg_calib_reduce(const dfg_calib_params *cp, int32_t mode, double x0, double x1, double *out3,
+                     void *d_scratch, size_t scratch_bytes, void *stream);
+DFG_API int dfg_calib_samples(const dfg_calib_params *cp, double *d_b, double *d_a, void *stream);
 
 #ifdef __cplusplus
 }

@@ -17,6 +17,7 @@ from .filters import (
     fixup_counts,
     last_fixup_count,
 )
+from .calibration import LinearFit, fit_angular_chromaticity, fit_line, sample_angle_chromaticity_pairs
 from .metrics import MetricsReport, compare, mae, metrics_device, ncd, psnr
 from .noise import NoiseParams, corrupt_device, corrupt_image
 from .image import REFLECT, REPLICATE, BorderPolicy, ColorVector, RasterImage, to_uint8
@@ -45,4 +46,5 @@ __all__ = [
     "filter_host", "filter_rows_device", "fixup_counts", "last_fixup_count", "parse_filter_spec", "to_uint8",
     "MetricsReport", "compare", "mae", "psnr", "ncd", "metrics_device",
     "NoiseParams", "corrupt_device", "corrupt_image",
+    "LinearFit", "fit_angular_chromaticity", "fit_line", "sample_angle_chromaticity_pairs",
 ]

@@ -21,7 +21,7 @@ EXPORTS = (
     "dfg_abi_version", "dfg_last_error", "dfg_workspace_bytes", "dfg_filter",
     "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_fixup_count",
     "dfg_reset_counts", "dfg_debug_values", "dfg_cr_acos_host", "dfg_corrupt_image",
-    "dfg_image_metrics",
+    "dfg_image_metrics", "dfg_calib_scratch_bytes", "dfg_calib_reduce", "dfg_calib_samples",
 )
 
 
@@ -50,6 +50,17 @@ class DfgNoiseParams(ctypes.Structure):
         ("phi3", ctypes.c_double),
         ("impulse", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
+        ("state_hi", ctypes.c_uint64),
+        ("state_lo", ctypes.c_uint64),
+        ("inc_hi", ctypes.c_uint64),
+        ("inc_lo", ctypes.c_uint64),
+    ]
+
+
+class DfgCalibParams(ctypes.Structure):
+    _fields_ = [
+        ("pairs", ctypes.c_int64),
+        ("p", ctypes.c_double),
         ("state_hi", ctypes.c_uint64),
         ("state_lo", ctypes.c_uint64),
         ("inc_hi", ctypes.c_uint64),
@@ -86,9 +97,13 @@ def lib() -> ctypes.CDLL:
     L.dfg_cr_acos_host.restype = ctypes.c_double
     L.dfg_corrupt_image.argtypes = [vp, i32, i32, i64, vp, i64, ctypes.POINTER(DfgNoiseParams), vp]
     L.dfg_image_metrics.argtypes = [vp, vp, i32, i32, i64, i64, ctypes.POINTER(ctypes.c_double), vp, vp]
+    L.dfg_calib_scratch_bytes.restype = sz
+    L.dfg_calib_reduce.argtypes = [ctypes.POINTER(DfgCalibParams), i32, ctypes.c_double, ctypes.c_double,
+                                   ctypes.POINTER(ctypes.c_double), vp, sz, vp]
+    L.dfg_calib_samples.argtypes = [ctypes.POINTER(DfgCalibParams), vp, vp, vp]
     for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host",
                  "dfg_fixup_count", "dfg_reset_counts", "dfg_debug_values", "dfg_corrupt_image",
-                 "dfg_image_metrics"):
+                 "dfg_image_metrics", "dfg_calib_reduce", "dfg_calib_samples"):
         getattr(L, name).restype = ctypes.c_int
     if L.dfg_abi_version() != 1:
         raise RuntimeError("libdfg.so ABI version mismatch; rebuild")

@@ -38,3 +38,20 @@ for _ in range(n):
 ms = (time.perf_counter() - t) * 1e3 / n  # synchronous call (result read back)
 print(json.dumps({"kernel": "dfg_image_metrics", "shape": [H, W], "ms": round(ms, 4),
                   "Mpx_s": round(px / ms / 1e3, 1), "GB_s": round(6 * px / ms / 1e6, 1)}))
+
+# calibration fit at the paper's 10^8 pairs (three streamed passes)
+from paper_1009_0958_b200 import calibration  # noqa: E402
+import oracle  # noqa: E402
+
+calibration.fit_angular_chromaticity(10**6, 0)
+torch.cuda.synchronize()
+t = time.perf_counter()
+f = calibration.fit_angular_chromaticity(10**8, 0)
+ms = (time.perf_counter() - t) * 1e3
+print(json.dumps({"kernel": "dfg_calib (fit_angular_chromaticity)", "pairs": 10**8, "ms": round(ms, 2),
+                  "Mpairs_s": round(1e8 / ms / 1e3, 1), "slope": f.slope, "intercept": f.intercept}))
+t = time.perf_counter()
+want = oracle.calib_fit(*oracle.calib_samples(10**7, 0))
+cpu_ms = (time.perf_counter() - t) * 1e3
+print(json.dumps({"cpu numpy reference restatement": "calib_samples + calib_fit", "pairs": 10**7,
+                  "ms": round(cpu_ms, 1), "Mpairs_s": round(1e7 / cpu_ms / 1e3, 2)}))

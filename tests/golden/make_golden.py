@@ -166,11 +166,26 @@ def main() -> None:
         met.append([r.mae, r.psnr, r.ncd_x1000])
     arrays["metrics_ref"] = np.asarray(met, dtype=np.float64)
 
+    # calibration line (calibration.py:83-125): samples of a small draw and
+    # fitted lines for a few (pairs, seed, p, method)
+    from dirfilt.calibration import fit_angular_chromaticity, sample_angle_chromaticity_pairs
+    cb, ca = sample_angle_chromaticity_pairs(2000, 7, 2.0)
+    arrays["calib_b"], arrays["calib_a"] = cb, ca
+    cb3, ca3 = sample_angle_chromaticity_pairs(1500, 8, 3.0)
+    arrays["calib_b_p3"], arrays["calib_a_p3"] = cb3, ca3
+    calib_cases = [(10**4, 0, 2.0, "tls"), (10**5, 1, 2.0, "ols"), (20000, 3, 1.0, "tls"), (10**6, 0, 2.0, "tls")]
+    fits = []
+    for n, sd, pp, meth in calib_cases:
+        f = fit_angular_chromaticity(n, sd, pp, meth)
+        fits.append([f.slope, f.intercept, f.fit_error, f.mean_abs_residual, f.rms_orthogonal])
+    arrays["calib_fits"] = np.asarray(fits, dtype=np.float64)
+
     np.savez_compressed(HERE / "filters.npz", **arrays)
     (HERE / "manifest.json").write_text(json.dumps({"reference": "dirfilt 0.1.0 (/root/reference/pkg)",
                                                     "numpy": np.__version__, "cases": cases,
                                                     "noise_cases": noise_manifest,
-                                                    "metrics_pairs": pairs}, indent=1))
+                                                    "metrics_pairs": pairs,
+                                                    "calib_cases": calib_cases}, indent=1))
     print(f"{len(cases)} filter cases, {sum(a.nbytes for a in arrays.values())} bytes raw")
 
 
