@@ -58,6 +58,11 @@ extern "C" {
 #define DFG_BVDF 2
 #define DFG_DDF 3
 #define DFG_ACWDDF 4
+/* extensions: the reference's window-level centre-weighted
+ * filters applied to every window -- cwvmf(w, k, p) filters.py:331-337 and
+ * cwddf(w, k, p, strategy) filters.py:304-328; smoothing level k in `lam` */
+#define DFG_CWVMF 5
+#define DFG_CWDDF 6
 
 /* strategy: filters.py:37-82 DirectionalStrategy.kind, _engine.py:25-28 */
 #define DFG_EXACT 0
@@ -85,7 +90,7 @@ typedef struct dfg_params {
     double p;            /* Minkowski order: spec.p, or acwddf.p for ACWDDF (filters.py:398) */
     double asin_c[5];    /* ASIN polynomial a0..a4, zero-padded (minimax only) */
     double acos_c[5];    /* ACOS polynomial a0..a4, zero-padded (minimax only) */
-    int32_t lam;         /* ACWDDF smoothing level lambda (>= 1, lambda + 2 <= (n+1)/2) */
+    int32_t lam;         /* ACWDDF smoothing level lambda (>= 1, lambda + 2 <= (n+1)/2); CW*: k */
     int32_t reserved;
     double threshold;    /* ACWDDF switching threshold T */
     double slope;        /* chromaticity calibration (ACWDDF switching sum only) */

@@ -27,7 +27,9 @@ from .spec import (
     CALIBRATION_INTERCEPT,
     CALIBRATION_SLOPE,
     FAMILIES,
+    CW_FAMILIES,
     AcwddfParams,
+    CenterWeightedSpec,
     DirectionalStrategy,
     FastAcosTable,
     FilterSpec,
@@ -47,4 +49,5 @@ __all__ = [
     "MetricsReport", "compare", "mae", "psnr", "ncd", "metrics_device",
     "NoiseParams", "corrupt_device", "corrupt_image",
     "LinearFit", "fit_angular_chromaticity", "fit_line", "sample_angle_chromaticity_pairs",
+    "CW_FAMILIES", "CenterWeightedSpec",
 ]

@@ -12,7 +12,7 @@ from .spec import ACOS_COEFFICIENTS, ASIN_COEFFICIENTS
 LIB_PATH = Path(__file__).resolve().parent / "libdfg.so"
 
 DFG_OK, DFG_E_ARG, DFG_E_CUDA, DFG_E_UNSUP, DFG_E_WS = 0, -1, -2, -3, -4
-FAMILY_CODE = {"identity": 0, "vmf": 1, "bvdf": 2, "ddf": 3, "acwddf": 4}
+FAMILY_CODE = {"identity": 0, "vmf": 1, "bvdf": 2, "ddf": 3, "acwddf": 4, "cwvmf": 5, "cwddf": 6}
 STRATEGY_CODE = {"exact": 0, "minimax": 1, "chromaticity": 2}
 BORDER_CODE = {"replicate": 0, "reflect": 1}
 
@@ -135,7 +135,7 @@ def params_from_spec(spec, policy) -> DfgParams:
         raise ValueError(f"unknown engine family {fam!r}")
     prm.family = FAMILY_CODE[fam]
     kind = spec.strategy.kind
-    prm.strategy = STRATEGY_CODE[kind] if fam != "vmf" else 0
+    prm.strategy = STRATEGY_CODE[kind] if fam not in ("vmf", "cwvmf") else 0
     prm.window = int(spec.window)
     mode = getattr(policy, "mode", policy)
     prm.border = BORDER_CODE[mode]
@@ -145,9 +145,9 @@ def params_from_spec(spec, policy) -> DfgParams:
         prm.threshold = float(spec.acwddf.threshold)
     else:
         prm.p = float(spec.p)
-        prm.lam = 2
+        prm.lam = int(spec.k) if fam in ("cwvmf", "cwddf") else 2  # centre-weighted: smoothing level k
         prm.threshold = 10.8
-    if kind == "minimax" and fam != "vmf":
+    if kind == "minimax" and fam not in ("vmf", "cwvmf"):
         table = spec.strategy.table  # reference and this package both expose it
         if table is not None:
             cs, ca = table.asin_poly.coefficients, table.acos_poly.coefficients

@@ -36,7 +36,7 @@ constexpr size_t kWsHeader = 256;
 int validate(const dfg_params *p)
 {
     if (!p) return fail(DFG_E_ARG, "null params");
-    if (p->family < DFG_IDENTITY || p->family > DFG_ACWDDF) return fail(DFG_E_ARG, "unknown filter family");
+    if (p->family < DFG_IDENTITY || p->family > DFG_CWDDF) return fail(DFG_E_ARG, "unknown filter family");
     if (p->strategy < DFG_EXACT || p->strategy > DFG_CHROMA) return fail(DFG_E_ARG, "unknown strategy kind");
     if (p->border != DFG_REPLICATE && p->border != DFG_REFLECT) return fail(DFG_E_ARG, "unknown border mode");
     if (p->window < 3 || (p->window % 2) == 0) return fail(DFG_E_ARG, "window side must be odd and >= 3");
@@ -47,6 +47,10 @@ int validate(const dfg_params *p)
         if (p->lam < 1) return fail(DFG_E_ARG, "lambda must be >= 1");
         if (p->lam + 2 > d) return fail(DFG_E_ARG, "lambda + 2 exceeds the number of smoothing levels");
         if (!(p->threshold >= 0.0)) return fail(DFG_E_ARG, "threshold must be nonnegative");
+    }
+    if (p->family == DFG_CWVMF || p->family == DFG_CWDDF) {  // center_weight, filters.py:85-94
+        const int n = p->window * p->window, d = (n + 1) / 2;
+        if (p->lam < 1 || p->lam > d) return fail(DFG_E_ARG, "smoothing level k must be in [1, (n+1)/2]");
     }
     if (p->family != DFG_IDENTITY && p->window != 3 && p->window != 5 && p->window != 7)
         return fail(DFG_E_UNSUP, "this build supports window sides 3, 5 and 7");
@@ -121,6 +125,8 @@ cudaError_t launch_fast(const dfg_params *p, cudaStream_t st, const uint8_t *in,
         case DFG_VMF: return dfg_launch_s##S##_vmf(p->strategy, pc, st, in, out, kp);  \
         case DFG_BVDF: return dfg_launch_s##S##_bvdf(p->strategy, pc, st, in, out, kp); \
         case DFG_DDF: return dfg_launch_s##S##_ddf(p->strategy, pc, st, in, out, kp);  \
+        case DFG_CWVMF: return dfg_launch_s##S##_cwvmf(p->strategy, pc, st, in, out, kp); \
+        case DFG_CWDDF: return dfg_launch_s##S##_cwddf(p->strategy, pc, st, in, out, kp); \
         default: return dfg_launch_s##S##_acwddf(p->strategy, pc, st, in, out, kp);    \
         }                                                                              \
     }

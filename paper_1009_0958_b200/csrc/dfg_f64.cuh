@@ -257,7 +257,13 @@ __device__ static void pair_tables(const E64 *e, const FParams &fp, int t, int n
         int i = 0, rem = k;
         while (rem >= n - 1 - i) { rem -= n - 1 - i; i++; }
         const int j = i + 1 + rem;
-        if (needA) dA[k] = pairA<CR>(e[i], e[j], fp);
+        if (needA) {
+            // the window-level forms the centre-weighted filters come from
+            // (filters.py:296-337) special-case equal vectors under minimax:
+            // fast_acos(1) = a0 exactly (distance.py:217-218)
+            const bool cw_dup = (fp.family == FAM_CWDDF) && fp.strategy == ST_MINIMAX && same_col(e[i], e[j]);
+            dA[k] = cw_dup ? fp.cs[0] : pairA<CR>(e[i], e[j], fp);
+        }
         if (needL && !CR) dL[k] = mink64(e[i].raw, e[j].raw, fp.p);
     }
 }
@@ -269,8 +275,8 @@ __device__ static int decide64(const E64 *e, const FParams &fp, int lane, const 
 {
     const int s = fp.window, n = s * s, dc = (n - 1) / 2;
     const int fam = fp.family;
-    const bool needA = fam != FAM_VMF;
-    const bool needL = fam == FAM_VMF || fam == FAM_DDF || fam == FAM_ACWDDF;
+    const bool needA = fam != FAM_VMF && fam != FAM_CWVMF;
+    const bool needL = fam != FAM_BVDF;
     double aA[2] = {0, 0}, aL[2] = {0, 0}, AD[2] = {0, 0}, LD[2] = {0, 0};
     for (int sl = 0; sl < 2; sl++) {
         const int i = lane + 32 * sl;
@@ -301,6 +307,16 @@ __device__ static int decide64(const E64 *e, const FParams &fp, int lane, const 
     }
     if (fam == FAM_BVDF) {
         const Cand c = select64(aA, lane, n, e, &g);
+        *margin = g;
+        return c.i;
+    }
+    if (fam == FAM_CWVMF || fam == FAM_CWDDF) {
+        // filters.py:296-337: weight-1 = n - 2k + 1 on the centre column
+        const double w = (double)(n - 2 * fp.lam + 2 - 1);
+        double cw[2];
+        for (int sl = 0; sl < 2; sl++)
+            cw[sl] = fam == FAM_CWVMF ? aL[sl] + w * LD[sl] : (aA[sl] + w * AD[sl]) * (aL[sl] + w * LD[sl]);
+        const Cand c = select64(cw, lane, n, e, &g);
         *margin = g;
         return c.i;
     }

@@ -437,9 +437,10 @@ __device__ __forceinline__ float4 rawrec(float x, float y, float z, float aux)
 template <int S, int FAM, int OPT, int TR>
 struct Cfg {
     static constexpr int H = S / 2, N = S * S, DC = (N - 1) / 2;
-    static constexpr bool NEED_A = FAM != FAM_VMF;
-    static constexpr bool NEED_L = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
+    static constexpr bool NEED_A = FamT<FAM>::A;
+    static constexpr bool NEED_L = FamT<FAM>::L;
     static constexpr bool BOTH = NEED_A && NEED_L;
+    static constexpr bool CEN = FamT<FAM>::CEN;
     static constexpr int TW = 32, NT = TR * TW, TH = TR * OPT;
     static constexpr int RH = TH + 2 * H, RW = TW + 2 * H, RN = RH * RW;
     static constexpr int RN4 = (RN + 3) & ~3;
@@ -590,6 +591,21 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
         const float er2 = 2.f * er, eal = 2.f * ea * lmax;
         doubt = s0.doubtful(er2, eal) || s1.doubtful(er2, eal) || s2.doubtful(er2, eal) ||
                 fabsf(sv - kp.threshold) <= es || (fires && sd.doubtful(er2, eal));
+    } else if constexpr (FAM == FAM_CWDDF) {
+        // filters.py:296-328: argmin (A + w AD)(L + w LD), w = n - 2k + 1
+        const float w0 = kp.w[0];
+        float lmax = 0.f;
+        static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, fmaf(w0, LD(ic), L(ic))); });
+        const Pick s = pick<N, false>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
+                                      col, none, none);
+        kc = s.k1;
+        doubt = s.doubtful(2.f * er, 2.f * ea * lmax);
+    } else if constexpr (FAM == FAM_CWVMF) {
+        // filters.py:331-337: argmin L + w LD
+        const float w0 = kp.w[0];
+        const Pick s = pick<N, false>([&](auto ic) { return fmaf(w0, LD(ic), L(ic)); }, col, none, none);
+        kc = s.k1;
+        doubt = s.doubtful(er, 0.f);
     } else if constexpr (FAM == FAM_DDF) {
         float lmax = 0.f;
         static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, L(ic)); });
@@ -611,8 +627,8 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
 template <int FAM, int ST, int PC, bool ZC>
 __device__ __forceinline__ void pair_values2(const Pix &p, const Pair2 &q, const KParams &kp, P2 &da, P2 &dl)
 {
-    constexpr bool NA = FAM != FAM_VMF;
-    constexpr bool NL = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
+    constexpr bool NA = FamT<FAM>::A;
+    constexpr bool NL = FamT<FAM>::L;
     if (NA) {
         if (ST == ST_EXACT) da = angle_half2<ZC>(p, q);
         else if (ST == ST_MINIMAX) da = angle_minimax2(p, q, kp);
@@ -686,7 +702,7 @@ __device__ __forceinline__ void seg_stages(const float4 *sA, const float4 *sB, t
     using DT = typename C::DT;
     constexpr int H = C::H, N = C::N, DC = C::DC, RW = C::RW, RH = C::RH, RN = C::RN, NT = C::NT;
     constexpr int RWS = C::RWS, PADC = C::PADC, NDV = C::NDV;
-    constexpr bool ACW = FAM == FAM_ACWDDF;
+    constexpr bool CEN = C::CEN;
     constexpr bool BOTH = C::BOTH;
     DT *sP = sD + C::NPL * RN;  // S_+du [v][RN]
     DT *sM = sP + S * RN;       // S_-du [v][RN]
@@ -803,17 +819,15 @@ __device__ __forceinline__ void seg_stages(const float4 *sA, const float4 *sB, t
                             aL[o][i] += add;
                         }
                     }
-                    if constexpr (ACW) {  // centre-column stash: the pair (i, centre) itself
+                    if constexpr (CEN) {  // centre-column stash: the pair (i, centre) itself
                         if (i < DC && H - u == du) {
                             const int dv = H - v;
                             const int k = dv - dv0;
-                            const DT x = sD[k * RN + qi];
-                            cen[o][i] = *reinterpret_cast<const P2 *>(&x);
+                            cen[o][i] = sD[k * RN + qi];
                         } else if (i > DC && u - H == du) {
                             const int dv = v - H;
                             const int k = dv - dv0;
-                            const DT x = sD[k * RN + (ry0 + H) * RW + tx + H];
-                            cen[o][i] = *reinterpret_cast<const P2 *>(&x);
+                            cen[o][i] = sD[k * RN + (ry0 + H) * RW + tx + H];
                         }
                     }
                 }
@@ -831,7 +845,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     using DT = typename C::DT;
     constexpr int H = C::H, N = C::N, DC = C::DC, RW = C::RW, RH = C::RH, RN = C::RN, NT = C::NT, TH = C::TH;
     constexpr int RWS = C::RWS, PADC = C::PADC;
-    constexpr bool ACW = FAM == FAM_ACWDDF;
+    constexpr bool CEN = C::CEN;
     constexpr bool BOTH = C::BOTH;
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -898,7 +912,8 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     __syncthreads();
 
     // aggregates: BOTH -> packed (angular, Minkowski) pairs; else scalars
-    P2 ag[OPT][BOTH ? N : 1], cen[OPT][(BOTH && ACW) ? N : 1];
+    P2 ag[OPT][BOTH ? N : 1];
+    DT cen[OPT][CEN ? N : 1];  // centre column (angular, Minkowski) or (Minkowski)
     float aA[OPT][(C::NEED_A && !BOTH) ? N : 1], aL[OPT][(C::NEED_L && !BOTH) ? N : 1];
 #pragma unroll
     for (int o = 0; o < OPT; o++) {
@@ -908,7 +923,10 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             else if constexpr (C::NEED_A) aA[o][i] = kp.self_term;
             else aL[o][i] = 0.f;
         }
-        if constexpr (ACW) cen[o][DC] = pk2(kp.self_term, 0.f);
+        if constexpr (CEN) {
+            if constexpr (BOTH) cen[o][DC] = make_float2(kp.self_term, 0.f);
+            else cen[o][DC] = dt_zero(DT());
+        }
     }
 
     if constexpr (C::SEG) {
@@ -992,16 +1010,16 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                                 const P2 x = *reinterpret_cast<const P2 *>(&val);
                                 ag[o][i] = add2(ag[o][i], x);
                                 ag[o][j] = add2(ag[o][j], x);
-                                if constexpr (ACW) {
-                                    if (j == DC) cen[o][i] = x;
-                                    else if (i == DC) cen[o][j] = x;
-                                }
                             } else if constexpr (C::NEED_A) {
                                 aA[o][i] += val;
                                 aA[o][j] += val;
                             } else {
                                 aL[o][i] += val;
                                 aL[o][j] += val;
+                            }
+                            if constexpr (CEN) {
+                                if (j == DC) cen[o][i] = val;
+                                else if (i == DC) cen[o][j] = val;
                             }
                         }
                     }
@@ -1039,8 +1057,8 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             if constexpr (BOTH) {
                 auto A = [&](auto ic) { return lo2(ag[o][decltype(ic)::value]); };
                 auto L = [&](auto ic) { return hi2(ag[o][decltype(ic)::value]); };
-                auto AD = [&](auto ic) { if constexpr (ACW) return lo2(cen[o][decltype(ic)::value]); else return 0.f; };
-                auto LD = [&](auto ic) { if constexpr (ACW) return hi2(cen[o][decltype(ic)::value]); else return 0.f; };
+                auto AD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value].x; else return 0.f; };
+                auto LD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value].y; else return 0.f; };
                 select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, kc, doubt);
             } else if constexpr (C::NEED_A) {
                 auto V = [&](auto ic) { return aA[o][decltype(ic)::value]; };
@@ -1049,7 +1067,8 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             } else {
                 auto V = [&](auto ic) { return aL[o][decltype(ic)::value]; };
                 auto Z = [](auto) { return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, kc, doubt);
+                auto CD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value]; else return 0.f; };
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, col, kc, doubt);
             }
         }
 
@@ -1139,24 +1158,25 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
 
 // Per (window, family) launch shape: OPT outputs per thread (register
 // blocking), TR thread-rows per CTA, MINB CTAs per SM.  Register-resident
-// state per output is n (BVDF/VMF), 2n (DDF) or 4n (ACWDDF) floats.
+// state per output is n (BVDF/VMF), 2n (DDF, CWVMF) or 4n (ACWDDF, CWDDF) floats.
 template <int FAM, int ST, int PC>
 cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp);  // dfg_w3.cuh
 
 template <int S, int FAM>
 struct Shape {
-    static constexpr int AGG = (FAM == FAM_ACWDDF ? 4 : (FAM == FAM_DDF ? 2 : 1)) * S * S;
+    static constexpr int AGG =
+        ((FamT<FAM>::A ? 1 : 0) + (FamT<FAM>::L ? 1 : 0)) * (FamT<FAM>::CEN ? 2 : 1) * S * S;
     static constexpr int OPT = (S >= 5 && 2 * AGG + 32 <= 131) ? 2 : 1;
     static constexpr int REG = OPT * AGG + 56;  // registers per thread, estimated (aggregates + working set)
     // The register file is split per SM sub-partition (16K registers each),
     // so the bound is warps per sub-partition, not per SM.
     static constexpr int WPS = 16384 / (REG * 32);
     static constexpr int TR0 = WPS >= 4 ? 8 : 4 * (WPS < 2 ? 2 : WPS);
-    static constexpr int TR = (S == 3 && FAM != FAM_ACWDDF) ? 16 : TR0;  // 16 warps x 2 CTAs, 64 registers
+    static constexpr int TR = (S == 3 && !FamT<FAM>::CEN) ? 16 : TR0;  // 16 warps x 2 CTAs, 64 registers
     static constexpr int MINB0 = WPS >= 4 ? (WPS / 2 > 4 ? 4 : WPS / 2) : 1;
     // 3x3 BVDF/DDF/VMF: 4 CTAs (32 warps) per SM hide the staging and
     // barrier latency better than the few extra registers would
-    static constexpr int MINB = (S == 3 && FAM != FAM_ACWDDF) ? 2 : MINB0;
+    static constexpr int MINB = (S == 3 && !FamT<FAM>::CEN) ? 2 : MINB0;
 };
 
 template <int S, int FAM, int ST, int PC>
@@ -1208,6 +1228,14 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
                                       const dfg::KParams &kp)                       \
     {                                                                               \
         DFG_P_SWITCH(S, dfg::FAM_VMF, dfg::ST_EXACT)                                \
+    }
+
+#define DFG_DEFINE_LAUNCH_CWVMF(S)                                                  \
+    cudaError_t dfg_launch_s##S##_cwvmf(int, int pcode, cudaStream_t st,            \
+                                        const uint8_t *in, uint8_t *out,            \
+                                        const dfg::KParams &kp)                     \
+    {                                                                               \
+        DFG_P_SWITCH(S, dfg::FAM_CWVMF, dfg::ST_EXACT)                              \
     }
 
 #define DFG_DEFINE_LAUNCH_BVDF(S)                                                   \

@@ -9,7 +9,17 @@
 
 namespace dfg {
 
-enum { FAM_VMF = 1, FAM_BVDF = 2, FAM_DDF = 3, FAM_ACWDDF = 4 };
+enum { FAM_VMF = 1, FAM_BVDF = 2, FAM_DDF = 3, FAM_ACWDDF = 4, FAM_CWVMF = 5, FAM_CWDDF = 6 };
+
+// What a family needs: angular aggregates (A), Minkowski aggregates (L), and
+// the centre column d(i, centre) (CEN: ACWDDF, and the centre-weighted
+// CWVMF / CWDDF of filters.py:296-337).
+template <int FAM>
+struct FamT {
+    static constexpr bool A = FAM != FAM_VMF && FAM != FAM_CWVMF;
+    static constexpr bool L = FAM != FAM_BVDF;
+    static constexpr bool CEN = FAM == FAM_ACWDDF || FAM == FAM_CWVMF || FAM == FAM_CWDDF;
+};
 enum { ST_EXACT = 0, ST_MINIMAX = 1, ST_CHROMA = 2 };
 enum { PC_2 = 0, PC_1 = 1, PC_GEN = 2 };  // Minkowski order: p == 2, p == 1, general
 
@@ -37,7 +47,7 @@ struct KParams {
     float cs[5], ca[5];
     float self_term;
     float slope, intercept, threshold;
-    float w[3];  // ACWDDF extra centre weights n - 2k + 1, k = lam..lam+2
+    float w[3];  // extra centre weights n - 2k + 1: ACWDDF k = lam..lam+2; CWVMF/CWDDF k = lam (w[0])
     // rigorous error budget of one FP32 aggregate against the reference's
     // float64 value: |agg32 - agg64| <= er * |agg| + ea   (angular term);
     // Minkowski aggregates carry er only.  ea_pair: one angular pair.
@@ -88,4 +98,10 @@ DFG_DECLARE_LAUNCH(7, vmf)
 DFG_DECLARE_LAUNCH(7, bvdf)
 DFG_DECLARE_LAUNCH(7, ddf)
 DFG_DECLARE_LAUNCH(7, acwddf)
+DFG_DECLARE_LAUNCH(3, cwvmf)
+DFG_DECLARE_LAUNCH(3, cwddf)
+DFG_DECLARE_LAUNCH(5, cwvmf)
+DFG_DECLARE_LAUNCH(5, cwddf)
+DFG_DECLARE_LAUNCH(7, cwvmf)
+DFG_DECLARE_LAUNCH(7, cwddf)
 

@@ -21,8 +21,8 @@ namespace dfg {
 
 template <int FAM>
 struct W3Cfg {
-    static constexpr bool NEED_A = FAM != FAM_VMF;
-    static constexpr bool NEED_L = FAM == FAM_VMF || FAM == FAM_DDF || FAM == FAM_ACWDDF;
+    static constexpr bool NEED_A = FamT<FAM>::A;
+    static constexpr bool NEED_L = FamT<FAM>::L;
     static constexpr bool BOTH = NEED_A && NEED_L;
     using DT = typename std::conditional<BOTH, float2, float>::type;
     static constexpr int WARPS = 2;
@@ -67,7 +67,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
 {
     using C = W3Cfg<FAM>;
     using DT = typename C::DT;
-    constexpr bool ACW = FAM == FAM_ACWDDF;
+    constexpr bool CEN = FamT<FAM>::CEN;
     constexpr bool BOTH = C::BOTH;
     constexpr int N = 9, DC = 4;
 
@@ -262,14 +262,18 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         const int oy = y - 1;
         if (oy < oy0) continue;  // warm-up rows (uniform across the warp)
         const bool valid = lane >= 1 && lane < 31 && oy < oy1 && col < kp.W;
-        P2 ag[BOTH ? N : 1], cen[ACW ? N : 1];
+        P2 ag[BOTH ? N : 1];
+        DT cen[CEN ? N : 1];  // centre column
         float aS[BOTH ? 1 : N];
 #pragma unroll
         for (int i = 0; i < N; i++) {
             if constexpr (BOTH) ag[i] = pk2(kp.self_term, 0.f);
             else aS[i] = C::NEED_A ? kp.self_term : 0.f;
         }
-        if constexpr (ACW) cen[DC] = pk2(kp.self_term, 0.f);
+        if constexpr (CEN) {
+            if constexpr (BOTH) cen[DC] = make_float2(kp.self_term, 0.f);
+            else cen[DC] = 0.f;
+        }
         const int lc = min(max(lane, 1), 30);  // clamp so lanes 0/31 read in-bounds (results unused)
         // ring rows of the window's input rows oy-1, oy, oy+1 (slots of y-2, y-1, y)
         const int s0 = sl2, s1 = sl1, s2 = sl0;
@@ -288,13 +292,13 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                     const P2 x = *reinterpret_cast<const P2 *>(&val);
                     ag[i] = add2(ag[i], x);
                     ag[j] = add2(ag[j], x);
-                    if constexpr (ACW) {
-                        if (j == DC) cen[i] = x;
-                        else if (i == DC) cen[j] = x;
-                    }
                 } else {
                     aS[i] += val;
                     aS[j] += val;
+                }
+                if constexpr (CEN) {
+                    if (j == DC) cen[i] = val;
+                    else if (i == DC) cen[j] = val;
                 }
             }
         }
@@ -309,13 +313,14 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
             if constexpr (BOTH) {
                 auto A = [&](auto ic) { return lo2(ag[decltype(ic)::value]); };
                 auto L = [&](auto ic) { return hi2(ag[decltype(ic)::value]); };
-                auto AD = [&](auto ic) { if constexpr (ACW) return lo2(cen[decltype(ic)::value]); else return 0.f; };
-                auto LD = [&](auto ic) { if constexpr (ACW) return hi2(cen[decltype(ic)::value]); else return 0.f; };
+                auto AD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value].x; else return 0.f; };
+                auto LD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value].y; else return 0.f; };
                 select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, cb, doubt);
             } else {
                 auto V = [&](auto ic) { return aS[decltype(ic)::value]; };
                 auto Z = [](auto) { return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, cb, doubt);
+                auto CD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value]; else return 0.f; };
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, col, cb, doubt);
             }
         }
         uint8_t *orow = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch;

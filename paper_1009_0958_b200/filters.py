@@ -92,6 +92,10 @@ def _validate_spec(spec) -> None:
     w = int(spec.window)
     if w < 3 or w % 2 == 0:
         raise ValueError(f"window side must be odd and >= 3, got {w}")
+    if fam in ("cwvmf", "cwddf"):
+        from .spec import center_weight
+
+        center_weight(w * w, int(spec.k))
     if fam == "acwddf":
         if spec.acwddf is None:
             raise ValueError("acwddf parameters are required exactly when family is acwddf")

@@ -213,6 +213,54 @@ class FilterSpec:
         return self.name
 
 
+CW_FAMILIES = ("cwvmf", "cwddf")
+
+
+@dataclass(frozen=True)
+class CenterWeightedSpec:
+    """Extension: the reference's window-level
+    centre-weighted filters applied to every window of an image --
+    ``cwvmf(w, k, p)`` (reference filters.py:331-337, weighted Minkowski sums
+    only) and ``cwddf(w, k, p, strategy)`` (filters.py:304-328, weighted
+    angular x Minkowski sums).  ``k`` is the smoothing level of
+    ``center_weight(n, k)``: k = 1 pins the centre, k = (n+1)/2 is the plain
+    filter.  Accepted by ``apply_filter`` like a ``FilterSpec``."""
+
+    family: str
+    k: int
+    strategy: DirectionalStrategy = field(default_factory=DirectionalStrategy.exact)
+    p: float = 2.0
+    window: int = 3
+    acwddf: Optional[AcwddfParams] = None  # always None (FilterSpec field parity)
+
+    def __post_init__(self) -> None:
+        if self.family not in CW_FAMILIES:
+            raise ValueError(f"unknown centre-weighted family {self.family!r} (choose from {CW_FAMILIES})")
+        if not self.p >= 1.0:
+            raise ValueError(f"Minkowski order must be >= 1, got {self.p}")
+        if self.window < 3 or self.window % 2 == 0:
+            raise ValueError(f"window side must be odd and >= 3, got {self.window}")
+        if self.acwddf is not None:
+            raise ValueError("centre-weighted specs carry no acwddf parameters")
+        center_weight(self.window * self.window, self.k)  # validates k
+
+    @property
+    def name(self) -> str:
+        out = [self.family, f"k={self.k}"]
+        if self.family == "cwddf":
+            out.append(self.strategy.token)
+            if self.strategy.kind == "minimax":
+                out.append(f"q={self.strategy.q}")
+        if self.p != 2.0:
+            out.append(f"p={_num(self.p)}")
+        if self.window != 3:
+            out.append(f"window={self.window}")
+        return ":".join(out)
+
+    def __str__(self) -> str:
+        return self.name
+
+
 def _num(x: float) -> str:
     x = float(x)
     return str(int(x)) if x == int(x) else repr(x)

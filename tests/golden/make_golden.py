@@ -180,12 +180,45 @@ def main() -> None:
         fits.append([f.slope, f.intercept, f.fit_error, f.mean_abs_residual, f.rms_orthogonal])
     arrays["calib_fits"] = np.asarray(fits, dtype=np.float64)
 
+    # centre-weighted filters (filters.py:296-337) applied to every window via
+    # the reference's extract_window (image.py:179-200)
+    from dirfilt.filters import cwddf, cwvmf
+    from dirfilt.image import extract_window
+    cw_cases = []
+    cw_specs = [("cwvmf", 1, "ddf:exact", 2.0, 3), ("cwvmf", 3, "ddf:exact", 2.0, 3), ("cwvmf", 2, "ddf:exact", 1.0, 3),
+                ("cwvmf", 5, "ddf:exact", 2.0, 3), ("cwvmf", 7, "ddf:exact", 2.0, 5), ("cwvmf", 4, "ddf:exact", 3.0, 5),
+                ("cwddf", 1, "ddf:exact", 2.0, 3), ("cwddf", 2, "ddf:exact", 2.0, 3), ("cwddf", 4, "ddf:minimax", 2.0, 3),
+                ("cwddf", 3, "ddf:minimax:q=2", 2.0, 3), ("cwddf", 2, "ddf:rgb", 2.0, 3), ("cwddf", 5, "ddf:exact", 2.0, 3),
+                ("cwddf", 6, "ddf:exact", 2.0, 5), ("cwddf", 9, "ddf:minimax", 2.0, 5), ("cwddf", 3, "ddf:rgb", 1.0, 5),
+                ("cwddf", 13, "ddf:exact", 2.0, 5), ("cwddf", 10, "ddf:exact", 2.0, 7)]
+    for ci, (fam, k, stext, pp, win) in enumerate(cw_specs):
+        for border in ("replicate", "reflect"):
+            h, w = (11, 13) if win < 7 else (9, 10)
+            img = synth.noisy_image(h, w, 500 + ci, ("correlated", 0.25))
+            img[2:4, 3:6] = 0
+            img[6:8, 1:3] = img[0, 0]  # duplicate colours (minimax a == b rule)
+            ref = RasterImage(img.astype(np.float64))
+            strat = parse_filter_spec(stext).strategy
+            pol = BorderPolicy(border)
+            out = np.zeros_like(img)
+            for r in range(h):
+                for c in range(w):
+                    wv = extract_window(ref, r + 1, c + 1, win, pol)
+                    v = cwvmf(wv, k, pp) if fam == "cwvmf" else cwddf(wv, k, pp, strat)
+                    out[r, c] = (int(v.x1), int(v.x2), int(v.x3))
+            i = len(cw_cases)
+            arrays[f"cw_in{i}"] = img
+            arrays[f"cw_out{i}"] = out
+            cw_cases.append({"family": fam, "k": k, "strategy": stext.split(":", 1)[1], "p": pp, "window": win,
+                             "border": border})
+
     np.savez_compressed(HERE / "filters.npz", **arrays)
     (HERE / "manifest.json").write_text(json.dumps({"reference": "dirfilt 0.1.0 (/root/reference/pkg)",
                                                     "numpy": np.__version__, "cases": cases,
                                                     "noise_cases": noise_manifest,
                                                     "metrics_pairs": pairs,
-                                                    "calib_cases": calib_cases}, indent=1))
+                                                    "calib_cases": calib_cases,
+                                                    "cw_cases": cw_cases}, indent=1))
     print(f"{len(cases)} filter cases, {sum(a.nbytes for a in arrays.values())} bytes raw")
 
 

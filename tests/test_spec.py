@@ -100,3 +100,14 @@ def test_uint8_boundary_conversion():
     for bad in (0.5, 256.0, -1.0, np.inf):
         with pytest.raises(ValueError):
             to_uint8(np.full((1, 1, 3), bad))
+
+
+def test_centre_weighted_spec_validation():
+    from paper_1009_0958_b200 import CenterWeightedSpec, DirectionalStrategy
+    s = CenterWeightedSpec("cwddf", 3, DirectionalStrategy.minimax(2), window=5)
+    assert s.name == "cwddf:k=3:minimax:q=2:window=5"
+    assert CenterWeightedSpec("cwvmf", 1).name == "cwvmf:k=1"
+    for bad in (dict(family="vmf", k=1), dict(family="cwvmf", k=0), dict(family="cwvmf", k=6),
+                dict(family="cwddf", k=2, p=0.5), dict(family="cwddf", k=2, window=4)):
+        with pytest.raises(ValueError):
+            CenterWeightedSpec(**bad)
