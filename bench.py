@@ -369,7 +369,7 @@ def run_ours(args, config):
     fma_px, mufu_px = WORK[config]
     px_per_s_gpu = wl["px"] / (ms_step / 1e3)
     achieved = px_per_s_gpu * fma_px / 1e12
-    traffic, traffic_src = None, None
+    traffic, traffic_src, pipes = None, None, None
     if world == 1:  # DRAM bytes per launch of this config's kernel, from the round's ncu --set full capture
         for tf in sorted(ROOT.glob("profiles/r*_traffic.json"), reverse=True):
             try:
@@ -378,12 +378,18 @@ def run_ours(args, config):
                 t = None
             if t:
                 traffic, traffic_src = int(t["dram_bytes"]), f"{tf.relative_to(ROOT)}: {t['kernel'][:60]}"
+                pipes = {k: round(t[k], 1) for k in ("fma_pipe_cycles_active_pct", "fma_pipe_inst_pct",
+                                                     "xu_pipe_inst_pct", "issue_active_pct") if k in t}
                 break
     roofline = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak_fma / 1e12, 3),
                 "unit": "T FMA-pipe lane-ops/s", "frac": round(achieved * 1e12 / peak_fma, 4), "traffic": traffic,
                 "traffic_note": (f"dram read+write bytes per launch (ncu, {traffic_src}); algorithmic "
                                  f"{BYTES_PER_PX * wl['px']} B per launch") if traffic else None,
                 "per_px": {"fma": fma_px, "mufu": mufu_px},
+                "ncu_issue": ({**pipes, "note": "measured FP32 (FMA pipe) / SFU (XU) issue utilisation of this "
+                               "config's kernel in the round's ncu capture -- the north star's 'achieved FP32/SFU "
+                               "issue rate against peak'; frac above credits only the canonical paper-formula work"}
+                              if pipes else None),
                 "note": "SURVEY 8(d) canonical work per pixel / device time of the step's single kernel (FP32 "
                         f"decision + in-kernel float64 re-decision); peak = 148 SM x 128 lanes x {sm_mhz:.0f} MHz "
                         f"({peak_src})",

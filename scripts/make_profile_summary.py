@@ -73,11 +73,15 @@ for rep in reps:
         def num(k):
             v, u = d[k]
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e-6, "msecond": 1e-3,
-                     "nsecond": 1e-9, "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1}.get(u.strip(), 1)
+                     "nsecond": 1e-9, "second": 1, "us": 1e-6, "ms": 1e-3, "ns": 1e-9, "s": 1, "%": 1}.get(u.strip(), 1)
             return float(v.replace(",", "")) * scale
         traffic[Path(rep).stem.replace("prof_", "")] = {
             "kernel": name, "dram_bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
-            "duration_s": num("gpu__time_duration.sum")}
+            "duration_s": num("gpu__time_duration.sum"),
+            "fma_pipe_cycles_active_pct": num("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+            "fma_pipe_inst_pct": num("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active"),
+            "xu_pipe_inst_pct": num("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+            "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active")}
     except (KeyError, ValueError):
         pass
 Path(f"profiles/{tag}_summary.md").write_text("\n".join(out) + "\n")
