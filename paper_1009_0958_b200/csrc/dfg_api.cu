@@ -188,6 +188,10 @@ int run(const uint8_t *d_in, int global_H, int W, int in_row0, int in_rows, long
     fill_params(prm, kp);
     kp.flag_count = (unsigned *)ws;
     kp.dbg = dbg;
+    {
+        const char *dg = getenv("DFG_DIAG_NO_FIXUP");  // diagnostics only
+        kp.diag_no_fixup = (dg && dg[0] == '1') ? 1 : 0;
+    }
     kp.w3_rpc = w3_rpc;
     kp.hostio = hostio;
 

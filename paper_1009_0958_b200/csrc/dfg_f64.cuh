@@ -226,7 +226,9 @@ __device__ static inline Cand select64(const double v[2], int lane, int n, const
     double other = INF;
     for (int s = 0; s < 2; s++) {
         const int i = lane + 32 * s;
-        if (i < n && !same_col(e[i], e[c.i]) && v[s] < other) other = v[s];
+        // exact zeros tie exactly with an exact-zero winner (first index wins
+        // in the reference too): not competitors for the margin
+        if (i < n && !same_col(e[i], e[c.i]) && v[s] > 0.0 && v[s] < other) other = v[s];
     }
     other = warp_min(other);
     const double den = fmax(fabs(c.v), fabs(other));

@@ -523,7 +523,13 @@ struct Pick {
     }
 };
 
-template <int N, bool PAY, typename FV, typename FC, typename FA, typename FL>
+// ZX: an FP32 value of exactly 0 is the reference's exact 0 (exact and
+// chromaticity routes: a zero pair value means parallel vectors, which the
+// reference also maps to exactly 0), so exact-zero competitors tie with an
+// exact-zero winner exactly -- the first index wins in both -- and are not
+// counted as competitors.  (A near-zero FP32 value the reference may round to
+// 0 stays a competitor: the absolute bound flags it.)
+template <int N, bool PAY, bool ZX, typename FV, typename FC, typename FA, typename FL>
 __device__ __forceinline__ Pick pick(FV val, FC col, FA pa, FL pl)
 {
     Pick r;
@@ -548,7 +554,7 @@ __device__ __forceinline__ Pick pick(FV val, FC col, FA pa, FL pl)
     });
     r.other = __int_as_float(0x7f800000);
     static_for<0, N>([&](auto ic) {
-        if (col(ic) != r.k1) r.other = fminf(r.other, val(ic));
+        if (col(ic) != r.k1 && (!ZX || val(ic) > 0.f)) r.other = fminf(r.other, val(ic));
     });
     return r;
 }
@@ -562,17 +568,18 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
                                               bool &doubt)
 {
     const float er = kp.er, ea = kp.ea;
+    constexpr bool ZX = ST != ST_MINIMAX;
     auto none = [](auto) { return 0.f; };
     if constexpr (FAM == FAM_ACWDDF) {
         const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
         float lmax = 0.f;  // largest Minkowski factor of any product (w0 >= w1 >= w2 >= 0)
         static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, fmaf(w0, LD(ic), L(ic))); });
-        const Pick sd = pick<N, false>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
-        const Pick s0 = pick<N, true>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
+        const Pick sd = pick<N, false, ZX>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
+        const Pick s0 = pick<N, true, ZX>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
                                       col, AD, LD);
-        const Pick s1 = pick<N, true>([&](auto ic) { return fmaf(w1, AD(ic), A(ic)) * fmaf(w1, LD(ic), L(ic)); },
+        const Pick s1 = pick<N, true, ZX>([&](auto ic) { return fmaf(w1, AD(ic), A(ic)) * fmaf(w1, LD(ic), L(ic)); },
                                       col, AD, LD);
-        const Pick s2 = pick<N, true>([&](auto ic) { return fmaf(w2, AD(ic), A(ic)) * fmaf(w2, LD(ic), L(ic)); },
+        const Pick s2 = pick<N, true, ZX>([&](auto ic) { return fmaf(w2, AD(ic), A(ic)) * fmaf(w2, LD(ic), L(ic)); },
                                       col, AD, LD);
         float a = s0.xa;
         if (ST == ST_CHROMA) a = fmaf(kp.slope, a, kp.intercept);
@@ -596,28 +603,28 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
         const float w0 = kp.w[0];
         float lmax = 0.f;
         static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, fmaf(w0, LD(ic), L(ic))); });
-        const Pick s = pick<N, false>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
+        const Pick s = pick<N, false, ZX>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
                                       col, none, none);
         kc = s.k1;
         doubt = s.doubtful(2.f * er, 2.f * ea * lmax);
     } else if constexpr (FAM == FAM_CWVMF) {
         // filters.py:331-337: argmin L + w LD
         const float w0 = kp.w[0];
-        const Pick s = pick<N, false>([&](auto ic) { return fmaf(w0, LD(ic), L(ic)); }, col, none, none);
+        const Pick s = pick<N, false, ZX>([&](auto ic) { return fmaf(w0, LD(ic), L(ic)); }, col, none, none);
         kc = s.k1;
         doubt = s.doubtful(er, 0.f);
     } else if constexpr (FAM == FAM_DDF) {
         float lmax = 0.f;
         static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, L(ic)); });
-        const Pick s = pick<N, false>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
+        const Pick s = pick<N, false, ZX>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
         kc = s.k1;
         doubt = s.doubtful(2.f * er, 2.f * ea * lmax);
     } else if constexpr (FAM == FAM_BVDF) {
-        const Pick s = pick<N, false>(A, col, none, none);
+        const Pick s = pick<N, false, ZX>(A, col, none, none);
         kc = s.k1;
         doubt = s.doubtful(er, ea);
     } else {
-        const Pick s = pick<N, false>(L, col, none, none);
+        const Pick s = pick<N, false, ZX>(L, col, none, none);
         kc = s.k1;
         doubt = s.doubtful(er, 0.f);
     }
@@ -1093,7 +1100,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             op[1] = (uint8_t)((col >> 8) & 0xff);
             op[2] = (uint8_t)((col >> 16) & 0xff);
         }
-        if (valid && doubt) {
+        if (valid && doubt && !kp.diag_no_fixup) {
             const unsigned slot = atomicAdd(&s_nflag, 1u);
             s_flag[slot] = (uint16_t)((ry0 << 5) | tx);
         }

@@ -64,6 +64,9 @@ struct KParams {
     int w3_rpc;
     // 1: in / out are mapped pinned host buffers (3x3 zero-copy host path)
     int hostio;
+    // diagnostics only (DFG_DIAG_NO_FIXUP=1): skip the float64 re-decision,
+    // to time its share -- results may then differ from the reference
+    int diag_no_fixup;
 };
 
 // Border policy resolution (image.py:158-176): replicate = clamp,

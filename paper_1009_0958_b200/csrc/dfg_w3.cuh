@@ -344,7 +344,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
             op[2] = (uint8_t)((cb >> 16) & 0xff);
         }
         // ---- 4. float64 re-decision of doubtful pixels (whole warp) -------
-        unsigned mask = __ballot_sync(0xffffffffu, valid && doubt);
+        unsigned mask = __ballot_sync(0xffffffffu, valid && doubt && !kp.diag_no_fixup);
         if (mask) {
             if (lane == 0) atomicAdd(kp.flag_count, (unsigned)__popc(mask));
             E64 *e64 = reinterpret_cast<E64 *>(f64b);
