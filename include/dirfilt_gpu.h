@@ -100,8 +100,11 @@ typedef struct dfg_params {
 DFG_API int dfg_abi_version(void);
 DFG_API const char *dfg_last_error(void);
 
-/* Device workspace needed to filter up to n_pixels output pixels per call
- * (diagnostic counters only; zero it once after allocation). */
+/* Device workspace needed to filter up to n_pixels output pixels per call:
+ * diagnostic counters and the 3x3 row sweep's deferred float64 re-decision
+ * queue.  Zero it once after allocation (every call leaves its queue state
+ * reset).  A workspace serves one call at a time: calls that may run
+ * concurrently (different streams) need separate workspaces. */
 DFG_API size_t dfg_workspace_bytes(int64_t n_pixels);
 
 /* Whole image: d_in (H, W, 3) -> d_out (H, W, 3), both device memory. */

@@ -29,6 +29,10 @@ int cuda_fail(cudaError_t e, const char *where)
 }
 
 constexpr size_t kWsHeader = 256;
+// deferred float64 re-decision queue of the 3x3 row sweep (16-byte entries
+// after the header): at most this many doubtful pixels per call are queued,
+// the rest are re-decided inline
+constexpr int64_t kQueueCap = 1 << 16;
 
 // Mirrors the reference's validation (filters.py:53-59, 110-123, 141-151,
 // image.py:44-46): invalid -> DFG_E_ARG (ValueError); valid but outside
@@ -191,9 +195,20 @@ int run(const uint8_t *d_in, int global_H, int W, int in_row0, int in_rows, long
     {
         const char *dg = getenv("DFG_DIAG_NO_FIXUP");  // diagnostics only
         kp.diag_no_fixup = (dg && dg[0] == '1') ? 1 : 0;
+        const char *dc = getenv("DFG_DIAG_CYCLES");  // diagnostics only
+        kp.diag_cycles = (dc && dc[0] == '1') ? 1 : 0;
     }
     kp.w3_rpc = w3_rpc;
     kp.hostio = hostio;
+    // the deferred queue needs the workspace to itself for the whole launch:
+    // not for the host pipeline's concurrent band kernels (w3_rpc > 0).
+    // Opt-in (DFG_W3_QUEUE=1): measured slower than the inline re-decision
+    // (the drain runs after the sweeps instead of overlapping them)
+    static const bool queue_env = [] {
+        const char *q = getenv("DFG_W3_QUEUE");
+        return q && q[0] == '1';
+    }();
+    kp.w3_queue = (queue_env && w3_rpc == 0 && !hostio) ? (int)(npx < kQueueCap ? npx : kQueueCap) : 0;
 
     cudaError_t e = launch_fast(prm, st, d_in, d_out, kp);
     if (e != cudaSuccess) return cuda_fail(e, "fast kernel launch");
@@ -257,8 +272,8 @@ const char *dfg_last_error(void) { return g_err.c_str(); }
 size_t dfg_workspace_bytes(int64_t n_pixels)
 {
     if (n_pixels < 0) n_pixels = 0;
-    (void)n_pixels;  // counters only: the float64 re-decision runs inside each CTA
-    return kWsHeader;
+    // counters + the 3x3 row sweep's re-decision queue
+    return kWsHeader + 16 * (size_t)(n_pixels < kQueueCap ? n_pixels : kQueueCap);
 }
 
 int dfg_filter(const uint8_t *d_in, int32_t H, int32_t W, int64_t in_pitch, uint8_t *d_out,

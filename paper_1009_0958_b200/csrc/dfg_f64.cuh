@@ -191,49 +191,9 @@ struct Cand {
     int i;
 };
 
-__device__ static inline Cand warp_argmin(Cand c)
-{
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, c.v, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, c.i, off);
-        if (ov < c.v || (ov == c.v && oi < c.i)) { c.v = ov; c.i = oi; }
-    }
-    return c;
-}
-
-__device__ static inline double warp_min(double v)
-{
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, off));
-    return v;
-}
-
 __device__ static inline bool same_col(const E64 &a, const E64 &b)
 {
     return a.raw[0] == b.raw[0] && a.raw[1] == b.raw[1] && a.raw[2] == b.raw[2];
-}
-
-// First strict minimum over the (up to 2 per lane) candidates + relative gap
-// to the best candidate of a different colour.
-__device__ static inline Cand select64(const double v[2], int lane, int n, const E64 *e, double *gap)
-{
-    const double INF = __longlong_as_double(0x7ff0000000000000LL);
-    Cand c = {INF, 1 << 20};
-    if (lane < n) c = {v[0], lane};
-    if (lane + 32 < n && v[1] < c.v) c = {v[1], lane + 32};
-    c = warp_argmin(c);
-    double other = INF;
-    for (int s = 0; s < 2; s++) {
-        const int i = lane + 32 * s;
-        // exact zeros tie exactly with an exact-zero winner (first index wins
-        // in the reference too): not competitors for the margin
-        if (i < n && !same_col(e[i], e[c.i]) && v[s] > 0.0 && v[s] < other) other = v[s];
-    }
-    other = warp_min(other);
-    const double den = fmax(fabs(c.v), fabs(other));
-    *gap = isinf(other) ? INF : (den == 0.0 ? 0.0 : (other - c.v) / den);
-    return c;
 }
 
 __device__ static inline double shfl_slot(const double v[2], int idx)
@@ -270,84 +230,184 @@ __device__ static void pair_tables(const E64 *e, const FParams &fp, int t, int n
     }
 }
 
-// Decide one window from the pair tables; returns the chosen index and the
-// smallest relative decision margin (argmin gaps, ACWDDF threshold margin).
-__device__ static int decide64(const E64 *e, const FParams &fp, int lane, const double *dA, const double *dL,
-                               double *margin)
+// Warp-sized variant for windows of N <= 2 x 32 pairs per lane (3x3: 36
+// pairs): each lane evaluates its pairs k = lane and lane + 32 in one
+// straight-line block (the second clamped to a valid pair, its store
+// predicated), so the two float64 chains overlap instead of running one
+// after the other -- the re-decision latency is what the row sweep waits on.
+template <bool CR, int N>
+__device__ static void pair_tables_warp(const E64 *e, const FParams &fp, int lane, double *dA, double *dL,
+                                        bool needA, bool needL)
 {
-    const int s = fp.window, n = s * s, dc = (n - 1) / 2;
-    const int fam = fp.family;
-    const bool needA = fam != FAM_VMF && fam != FAM_CWVMF;
-    const bool needL = fam != FAM_BVDF;
+    constexpr int P = N * (N - 1) / 2;
+    static_assert(P <= 64, "two pairs per lane at most");
+    int ii[2], jj[2];
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const int k = min(lane + 32 * r, P - 1);
+        int i = 0, rem = k;
+#pragma unroll
+        for (int q = 0; q < N - 1; q++)
+            if (rem >= N - 1 - i) { rem -= N - 1 - i; i++; }
+        ii[r] = i;
+        jj[r] = i + 1 + rem;
+    }
+    double va[2], vl[2];
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const E64 &a = e[ii[r]], &b = e[jj[r]];
+        if (needA) {
+            const bool cw_dup = (fp.family == FAM_CWDDF) && fp.strategy == ST_MINIMAX && same_col(a, b);
+            va[r] = cw_dup ? fp.cs[0] : pairA<CR>(a, b, fp);
+        }
+        if (needL && !CR) vl[r] = mink64(a.raw, b.raw, fp.p);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; r++) {
+        const int k = lane + 32 * r;
+        if (k < P) {
+            if (needA) dA[k] = va[r];
+            if (needL && !CR) dL[k] = vl[r];
+        }
+    }
+}
+
+// First strict minimum over the (up to 2 per lane) candidates of each of M
+// value sets, and whether the relative gap to the best candidate of a
+// different colour is below `margin` (no division: gap < margin  <=>
+// other - v < margin * den).  The M butterflies run interleaved (ACWDDF's
+// four selections cost one reduction's latency).
+template <int N, int M>
+__device__ static inline void select64m(const double (&v)[M][2], int lane, const E64 *e, double margin, Cand (&c)[M],
+                                        bool (&close)[M])
+{
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        c[m] = {INF, 1 << 20};
+        if (lane < N) c[m] = {v[m][0], lane};
+        if (lane + 32 < N && v[m][1] < c[m].v) c[m] = {v[m][1], lane + 32};
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int m = 0; m < M; m++) {
+            const double ov = __shfl_xor_sync(0xffffffffu, c[m].v, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, c[m].i, off);
+            if (ov < c[m].v || (ov == c[m].v && oi < c[m].i)) { c[m].v = ov; c[m].i = oi; }
+        }
+    }
+    double other[M];
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        other[m] = INF;
+#pragma unroll
+        for (int s = 0; s < (N + 31) / 32; s++) {
+            const int i = lane + 32 * s;
+            // exact zeros tie exactly with an exact-zero winner (first index
+            // wins in the reference too): not competitors for the margin
+            if (i < N && !same_col(e[i], e[c[m].i]) && v[m][s] > 0.0 && v[m][s] < other[m]) other[m] = v[m][s];
+        }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int m = 0; m < M; m++) other[m] = fmin(other[m], __shfl_xor_sync(0xffffffffu, other[m], off));
+    }
+#pragma unroll
+    for (int m = 0; m < M; m++) {
+        const double den = fmax(fabs(c[m].v), fabs(other[m]));
+        close[m] = !isinf(other[m]) && (den == 0.0 || other[m] - c[m].v < margin * den);
+    }
+}
+
+// Decide one window of N pixels from the pair tables (one warp; lane i and
+// i + 32 hold candidates i, i + 32): returns the chosen index and sets
+// *close when the smallest relative decision margin (argmin gaps, ACWDDF
+// threshold margin) is below fp.cr_margin -- the exact route's cue for the
+// correctly rounded pass.  Family, strategy and window are compile-time, so
+// the aggregate loops unroll with all table loads independent.
+template <int N, int FAM, int ST>
+__device__ static inline int decide64(const E64 *e, const FParams &fp, int lane, const double *dA, const double *dL,
+                                      bool *close)
+{
+    constexpr int dc = (N - 1) / 2;
+    constexpr bool needA = FAM != FAM_VMF && FAM != FAM_CWVMF;
+    constexpr bool needL = FAM != FAM_BVDF;
     double aA[2] = {0, 0}, aL[2] = {0, 0}, AD[2] = {0, 0}, LD[2] = {0, 0};
-    for (int sl = 0; sl < 2; sl++) {
+#pragma unroll
+    for (int sl = 0; sl < (N + 31) / 32; sl++) {
         const int i = lane + 32 * sl;
-        if (i >= n) continue;
-        // agg[i] = self + sum over j != i in ascending j (_engine.py:239-281)
+        if (i >= N) continue;
+        // agg[i] = self + sum over j != i in ascending j (_engine.py:239-281);
+        // pair (i, j), j > i: row i of the upper triangle; (j, i), j < i: row j
+        const int row_i = i * N - i * (i + 1) / 2 - i - 1;
         double a = fp.self_term, l = 0.0, ad = fp.self_term, ld = 0.0;
-        for (int j = 0; j < n; j++) {
-            if (j == i) continue;
-            const int k = i < j ? pair_index(i, j, n) : pair_index(j, i, n);
+#pragma unroll
+        for (int j = 0; j < N; j++) {
+            const int k = j < i ? j * N - j * (j + 1) / 2 + i - j - 1 : (j > i ? row_i + j : 0);
             if (needA) {
                 const double d = dA[k];
-                a += d;
-                if (j == dc) ad = d;
+                if (j != i) a += d;
+                if (j == dc && i != dc) ad = d;
             }
             if (needL) {
                 const double d = dL[k];
-                l += d;
-                if (j == dc) ld = d;
+                if (j != i) l += d;
+                if (j == dc && i != dc) ld = d;
             }
         }
         aA[sl] = a; aL[sl] = l; AD[sl] = ad; LD[sl] = ld;
     }
-    double g;
-    if (fam == FAM_VMF) {
-        const Cand c = select64(aL, lane, n, e, &g);
-        *margin = g;
-        return c.i;
+    const double cm = fp.cr_margin;
+    if constexpr (FAM == FAM_VMF || FAM == FAM_BVDF || FAM == FAM_DDF || FAM == FAM_CWVMF || FAM == FAM_CWDDF) {
+        double v[1][2];
+        for (int sl = 0; sl < 2; sl++) {
+            if constexpr (FAM == FAM_VMF) v[0][sl] = aL[sl];
+            else if constexpr (FAM == FAM_BVDF) v[0][sl] = aA[sl];
+            else if constexpr (FAM == FAM_DDF) v[0][sl] = aA[sl] * aL[sl];
+            else {
+                // filters.py:296-337: weight-1 = n - 2k + 1 on the centre column
+                const double w = (double)(N - 2 * fp.lam + 2 - 1);
+                v[0][sl] = FAM == FAM_CWVMF ? aL[sl] + w * LD[sl] : (aA[sl] + w * AD[sl]) * (aL[sl] + w * LD[sl]);
+            }
+        }
+        Cand c[1];
+        bool cl[1];
+        select64m<N, 1>(v, lane, e, cm, c, cl);
+        *close = cl[0];
+        return c[0].i;
+    } else {
+        // ACWDDF (_engine.py:451-487): the DDF pick and the centre-weighted
+        // picks for k = lam .. lam + 2, weights w_k = n - 2k + 2 - 1
+        double v[4][2];
+        for (int sl = 0; sl < 2; sl++) {
+            v[0][sl] = aA[sl] * aL[sl];
+#pragma unroll
+            for (int k = 0; k < 3; k++) {
+                const double w = (double)(N - 2 * (fp.lam + k) + 2 - 1);
+                v[1 + k][sl] = (aA[sl] + w * AD[sl]) * (aL[sl] + w * LD[sl]);
+            }
+        }
+        Cand c[4];
+        bool cl[4];
+        select64m<N, 4>(v, lane, e, cm, c, cl);
+        bool any = cl[1] || cl[2] || cl[3];
+        double sv = 0.0;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+            double a = shfl_slot(AD, c[1 + k].i);
+            const double l = shfl_slot(LD, c[1 + k].i);
+            if (ST == ST_CHROMA) a = fp.slope * a + fp.intercept;
+            sv += a * l;
+        }
+        const bool fires = sv > fp.threshold;
+        if (fires) any = any || cl[0];
+        const double den = fmax(fabs(sv), fabs(fp.threshold));
+        any = any || den == 0.0 || fabs(sv - fp.threshold) < cm * den;
+        *close = any;
+        return fires ? c[0].i : dc;
     }
-    if (fam == FAM_BVDF) {
-        const Cand c = select64(aA, lane, n, e, &g);
-        *margin = g;
-        return c.i;
-    }
-    if (fam == FAM_CWVMF || fam == FAM_CWDDF) {
-        // filters.py:296-337: weight-1 = n - 2k + 1 on the centre column
-        const double w = (double)(n - 2 * fp.lam + 2 - 1);
-        double cw[2];
-        for (int sl = 0; sl < 2; sl++)
-            cw[sl] = fam == FAM_CWVMF ? aL[sl] + w * LD[sl] : (aA[sl] + w * AD[sl]) * (aL[sl] + w * LD[sl]);
-        const Cand c = select64(cw, lane, n, e, &g);
-        *margin = g;
-        return c.i;
-    }
-    double pd[2] = {aA[0] * aL[0], aA[1] * aL[1]};
-    const Cand cd = select64(pd, lane, n, e, &g);
-    if (fam == FAM_DDF) {
-        *margin = g;
-        return cd.i;
-    }
-    // ACWDDF (_engine.py:451-487): weights w_k = n - 2k + 2 - 1
-    double gmin = __longlong_as_double(0x7ff0000000000000LL), sv = 0.0;
-    for (int k = 0; k < 3; k++) {
-        const double w = (double)(n - 2 * (fp.lam + k) + 2 - 1);
-        double cw[2];
-        for (int sl = 0; sl < 2; sl++) cw[sl] = (aA[sl] + w * AD[sl]) * (aL[sl] + w * LD[sl]);
-        double gk;
-        const Cand c = select64(cw, lane, n, e, &gk);
-        gmin = fmin(gmin, gk);
-        double a = shfl_slot(AD, c.i);
-        const double l = shfl_slot(LD, c.i);
-        if (fp.strategy == ST_CHROMA) a = fp.slope * a + fp.intercept;
-        sv += a * l;
-    }
-    const bool fires = sv > fp.threshold;
-    if (fires) gmin = fmin(gmin, g);
-    const double den = fmax(fabs(sv), fabs(fp.threshold));
-    gmin = fmin(gmin, den == 0.0 ? 0.0 : fabs(sv - fp.threshold) / den);
-    *margin = gmin;
-    return fires ? cd.i : dc;
 }
 
 }  // namespace dfg

@@ -863,7 +863,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     __shared__ unsigned s_nflag;          // this CTA's pixels needing float64 re-decision
     __shared__ uint16_t s_flag[TH * 32];  // (window top row << 5) | column
     __shared__ int s_b;
-    __shared__ double s_m;
+    __shared__ bool s_close;
 
     const int tid = threadIdx.x;
     const int tx = tid & 31, ty = tid >> 5;
@@ -1133,19 +1133,19 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         pair_tables<false>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
         __syncthreads();
         if (ty == 0) {
-            double m;
-            const int bb = decide64(e64, fp, tx, dA, dL, &m);
-            if (tx == 0) { s_b = bb; s_m = m; }
+            bool close;
+            const int bb = decide64<N, FAM, ST>(e64, fp, tx, dA, dL, &close);
+            if (tx == 0) { s_b = bb; s_close = close; }
         }
         __syncthreads();
-        if (ST == ST_EXACT && C::NEED_A && s_m < fp.cr_margin) {
+        if (ST == ST_EXACT && C::NEED_A && s_close) {
             // pass 2: correctly rounded arccos (dfg_f64.cuh)
             if (tid == 0) atomicAdd(kp.flag_count + 1, 1u);
             pair_tables<true>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
             __syncthreads();
             if (ty == 0) {
-                double m;
-                const int bb = decide64(e64, fp, tx, dA, dL, &m);
+                bool close;
+                const int bb = decide64<N, FAM, ST>(e64, fp, tx, dA, dL, &close);
                 if (tx == 0) s_b = bb;
             }
             __syncthreads();

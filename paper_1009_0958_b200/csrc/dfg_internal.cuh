@@ -67,6 +67,12 @@ struct KParams {
     // diagnostics only (DFG_DIAG_NO_FIXUP=1): skip the float64 re-decision,
     // to time its share -- results may then differ from the reference
     int diag_no_fixup;
+    // diagnostics only (DFG_DIAG_CYCLES=1): SM cycles spent in the float64
+    // re-decision, summed into the 64-bit counter at flag_count + 4
+    int diag_cycles;
+    // > 0: capacity (entries) of the 3x3 row sweep's deferred float64
+    // re-decision queue in the workspace (dfg_w3.cuh); 0: re-decide inline
+    int w3_queue;
 };
 
 // Border policy resolution (image.py:158-176): replicate = clamp,

@@ -48,11 +48,11 @@ struct W3Cfg {
 // du = 1 -> dv -2..2 (k 2..6); du = 2 -> dv -2..2 (k 7..11)
 __host__ __device__ constexpr int w3_k(int du, int dv) { return du == 0 ? dv - 1 : 2 + (du - 1) * 5 + (dv + 2); }
 
-// resident blocks per SM: 9 (18 warps, 96 registers) for the exact route;
-// the minimax route's two polynomials and the chromaticity route's sums
-// need more registers -> 8 (16 warps, 128 registers)
+// resident blocks per SM: 8 (16 warps, 128 registers) -- the launch sizes
+// its chunks for whole waves of 16 resident warps per SM (launch_w3);
+// measured: 18 or 20 resident warps (96 registers) run 10-14% slower
 template <int ST>
-constexpr int w3_minb() { return ST == ST_EXACT ? 9 : 8; }
+constexpr int w3_minb() { return 8; }
 
 // HIO (host I/O): `in` / `out` are mapped pinned HOST buffers -- the kernel
 // streams its rows over PCIe itself (the host path's zero-copy mode): each
@@ -60,9 +60,191 @@ constexpr int w3_minb() { return ST == ST_EXACT ? 9 : 8; }
 // bytes redistributed by shuffles) and written as aligned words assembled in
 // shared memory, so PCIe sees full coalesced requests in both directions
 // (full duplex) while the SMs compute.
-template <int FAM, int ST, int PC, bool HIO>
-__global__ void __launch_bounds__(64, w3_minb<ST>())
-dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const KParams kp, int n_strips,
+// Float64 re-decision of one window (whole warp): lane i < 9 holds the
+// packed colour of window pixel i; returns the chosen window index.
+template <int FAM, int ST>
+__device__ __forceinline__ int w3_decide64(const KParams &kp, unsigned char *f64b, uint32_t cc)
+{
+    using C = W3Cfg<FAM>;
+    constexpr int N = 9;
+    const int lane = threadIdx.x & 31;
+    E64 *e64 = reinterpret_cast<E64 *>(f64b);
+    double *dA = reinterpret_cast<double *>(e64 + N);
+    double *dL = dA + 36;
+    if (lane < N)
+        prep64(make_float4((float)(cc & 0xff), (float)((cc >> 8) & 0xff), (float)((cc >> 16) & 0xff), 0.f), ST,
+               e64[lane]);
+    __syncwarp();
+    pair_tables_warp<false, N>(e64, kp.fp, lane, dA, dL, C::NEED_A, C::NEED_L);
+    __syncwarp();
+    bool close;
+    int bb = decide64<N, FAM, ST>(e64, kp.fp, lane, dA, dL, &close);
+    if (ST == ST_EXACT && C::NEED_A && close) {
+        if (lane == 0) atomicAdd(kp.flag_count + 1, 1u);
+        __syncwarp();
+        pair_tables_warp<true, N>(e64, kp.fp, lane, dA, dL, C::NEED_A, C::NEED_L);
+        __syncwarp();
+        bb = decide64<N, FAM, ST>(e64, kp.fp, lane, dA, dL, &close);
+    }
+    __syncwarp();
+    return bb;
+}
+
+// Inline re-decision of the doubtful pixels `mask` of one output row segment
+// from the warp's ring (window row u of the output in ring slot sl[u]): the
+// host-I/O kernel, the host pipeline's band kernels and queue overflow.
+template <int FAM, int ST>
+__device__ __forceinline__ void w3_redecide(const KParams &kp, const uint32_t *rK, int sl0, int sl1, int sl2,
+                                         unsigned char *f64b, unsigned mask, uint8_t *orow_px)
+{
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) atomicAdd(kp.flag_count, (unsigned)__popc(mask));
+    const long long t0 = kp.diag_cycles ? clock64() : 0;
+    while (mask) {
+        const int fl = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int sr = lane < 3 ? sl2 : (lane < 6 ? sl1 : sl0);
+        const uint32_t cc = lane < 9 ? rK[sr * 32 + fl - 1 + lane % 3] : 0u;
+        const int bb = w3_decide64<FAM, ST>(kp, f64b, cc);
+        const uint32_t kb = __shfl_sync(0xffffffffu, cc, bb);
+        if (lane == 0) {
+            uint8_t *op = orow_px + 3 * (fl - 1);
+            op[0] = (uint8_t)(kb & 0xff);
+            op[1] = (uint8_t)((kb >> 8) & 0xff);
+            op[2] = (uint8_t)((kb >> 16) & 0xff);
+        }
+    }
+    if (kp.diag_cycles && lane == 0)
+        atomicAdd(reinterpret_cast<unsigned long long *>(kp.flag_count + 4), (unsigned long long)(clock64() - t0));
+}
+
+// Deferred re-decision queue (kp.w3_queue): the sweep appends its doubtful
+// pixels {frame, out row, column, state} to the workspace instead of
+// stalling its row sweep for the float64 work, and every warp drains the
+// queue after its sweep, so the re-decisions spread over the warps that
+// finish first instead of lengthening the sweeps of the warps that found
+// them (the single-wave grid ends with its slowest warp).
+//
+// Workspace words after the diagnostic counters: [8] entries appended,
+// [9] tickets drawn, [10] CTAs done.  Entry state: 0 empty, 1 published,
+// 2 abandoned.  A drainer draws ticket t only when the queue looked
+// non-empty, then resolves entry t with one compare-and-swap: published ->
+// it re-decides the pixel; still empty (it raced past the producers) -> it
+// marks the entry abandoned and stops, and the producer that later appends
+// at t finds the mark and re-decides that pixel itself.  No warp ever
+// waits on another, every entry is re-decided exactly once, and the last
+// CTA resets the counters and the abandoned marks for the next call.
+constexpr int kQueueWord = 8;
+constexpr int kQueueEntryOffset = 256;  // bytes: entries follow the counter header
+
+__device__ __forceinline__ uint4 *w3_queue_entries(const KParams &kp)
+{
+    return reinterpret_cast<uint4 *>(reinterpret_cast<unsigned char *>(kp.flag_count) + kQueueEntryOffset);
+}
+
+// Re-decide the pixel of one published entry (whole warp), reading its
+// window from the input image.
+template <int FAM, int ST>
+__device__ __forceinline__ void w3_redecide_entry(const KParams &kp, const uint8_t *in, uint8_t *out,
+                                               unsigned char *f64b, uint4 en)
+{
+    const int lane = threadIdx.x & 31;
+    const int frame = (int)en.x, oy = (int)en.y, col = (int)en.z;
+    // window pixel i = lane: input row of output row oy - 1 + i / 3, column col - 1 + i % 3
+    uint32_t cc = 0u;
+    if (lane < 9) {
+        int gy = kp.out_row0 + oy - 1 + lane / 3;
+        if ((unsigned)gy >= (unsigned)kp.global_H) gy = resolve_idx(gy, kp.global_H, kp.border);
+        const int ry = min(max(gy - kp.in_row0, 0), kp.in_rows - 1);
+        const int cx = resolve_idx(col - 1 + lane % 3, kp.W, kp.border);
+        const uint8_t *px = in + (long long)frame * kp.in_fstride + (long long)ry * kp.in_pitch + 3 * cx;
+        cc = (uint32_t)px[0] | ((uint32_t)px[1] << 8) | ((uint32_t)px[2] << 16);
+    }
+    const int bb = w3_decide64<FAM, ST>(kp, f64b, cc);
+    const uint32_t kb = __shfl_sync(0xffffffffu, cc, bb);
+    if (lane == 0) {
+        uint8_t *op = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch + 3 * col;
+        op[0] = (uint8_t)(kb & 0xff);
+        op[1] = (uint8_t)((kb >> 8) & 0xff);
+        op[2] = (uint8_t)((kb >> 16) & 0xff);
+    }
+}
+
+// Drain the queue (whole warp), then retire the warp (its CTA's last warp
+// counts the CTA done; the grid's last CTA resets the queue).
+template <int FAM, int ST>
+__device__ __forceinline__ void w3_drain(const KParams &kp, const uint8_t *in, uint8_t *out, unsigned char *f64b,
+                                      unsigned cta_warps, unsigned total_ctas, unsigned *s_done)
+{
+    const int lane = threadIdx.x & 31;
+    unsigned *qc = kp.flag_count + kQueueWord;
+    uint4 *qe = w3_queue_entries(kp);
+    const unsigned cap = (unsigned)kp.w3_queue;
+    const long long t0 = kp.diag_cycles ? clock64() : 0;
+    bool any = false;
+    for (;;) {
+        // lane 0: 0 = stop, 1 = entry t to re-decide
+        unsigned t = 0, go = 0;
+        uint4 en = make_uint4(0, 0, 0, 0);
+        if (lane == 0) {
+            const unsigned pr = *reinterpret_cast<volatile unsigned *>(qc);
+            const unsigned tk = *reinterpret_cast<volatile unsigned *>(qc + 1);
+            if (tk < min(pr, cap)) {
+                t = atomicAdd(qc + 1, 1u);
+                if (t < cap) {
+                    const unsigned old = atomicCAS(&qe[t].w, 0u, 2u);  // empty -> abandoned
+                    if (old == 1u) {                                   // published
+                        __threadfence();
+                        const volatile uint4 *ve = qe + t;
+                        en = make_uint4(ve->x, ve->y, ve->z, 0u);
+                        qe[t].w = 0u;  // consumed: clean for the next call
+                        go = 1;
+                    }
+                }
+            }
+        }
+        go = __shfl_sync(0xffffffffu, go, 0);
+        if (!go) break;
+        any = true;
+        en.x = __shfl_sync(0xffffffffu, en.x, 0);
+        en.y = __shfl_sync(0xffffffffu, en.y, 0);
+        en.z = __shfl_sync(0xffffffffu, en.z, 0);
+        w3_redecide_entry<FAM, ST>(kp, in, out, f64b, en);
+    }
+    if (lane == 0) {
+        if (kp.diag_cycles && any)
+            atomicAdd(reinterpret_cast<unsigned long long *>(kp.flag_count + 4), (unsigned long long)(clock64() - t0));
+        if (atomicAdd(s_done, 1u) == cta_warps - 1) {  // this CTA's last warp
+            __threadfence();
+            if (atomicAdd(qc + 2, 1u) == total_ctas - 1) {  // the grid's last CTA: reset
+                const unsigned pr = min(*reinterpret_cast<volatile unsigned *>(qc), cap);
+                const unsigned tk = min(*reinterpret_cast<volatile unsigned *>(qc + 1), cap);
+                for (unsigned i = pr; i < tk; i++) qe[i].w = 0u;  // tickets drawn past the last entry
+                qc[0] = 0u;
+                qc[1] = 0u;
+                qc[2] = 0u;
+                __threadfence();
+            }
+        }
+    }
+}
+
+// The row loop is unrolled by the ring period (3): in phase PH the current
+// row's ring slot is PH, the previous row's (PH + 2) % 3 and the one before
+// (PH + 1) % 3 -- compile-time slot addresses, no rotation moves.
+//
+// Aggregation by column sums (per window row t, for the lane's own pixel P_t
+// of that row): V_t(dv) = sum over the three window rows of d(P_t, (row,
+// col(P_t) + dv)), dv in -2..2; the aggregate of P_t in the window whose
+// columns are col(P_t) + {0,1,2} / {-1,0,1} / {-2,-1,0} is the sum of three
+// V's, and the outputs one lane right / here / one lane left receive those
+// by shuffles: 14 additions per window row (42 per output) instead of 72.
+// The values are the ring entries of the 36 window pairs' lower pixels, each
+// loaded by the lane of P_t (the sums cover every other window pixel once,
+// so the error budget's (n-1)-term summation bound holds unchanged).
+template <int FAM, int ST, int PC, bool HIO, int MINB>
+__global__ void __launch_bounds__(64, MINB)
+dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const __grid_constant__ KParams kp, int n_strips,
               int n_chunks)
 {
     using C = W3Cfg<FAM>;
@@ -72,7 +254,10 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
     constexpr int N = 9, DC = 4;
 
     extern __shared__ __align__(16) unsigned char w3_smem[];
+    __shared__ unsigned s_done;  // warps of this CTA done draining
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_done = 0;
+    __syncthreads();
     const int gw = blockIdx.x * C::WARPS + warp;  // global warp id within the frame
     if (gw >= n_strips * n_chunks) return;        // whole warp exits together
     const int strip = gw % n_strips, chunk = gw / n_strips;
@@ -155,17 +340,9 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
     // this lane's pixels of the previous two row steps (the vertical pair's
     // partners for lane l-2); neutral until the warm-up steps fill them
     Pix pm1 = {1.f, 1.f, 1.f, 1.f}, pm2 = {1.f, 1.f, 1.f, 1.f};
-    // ring slots of rows y, y-1, y-2 (rotated each step, no modulo)
-    int sl0 = 0, sl1 = 2, sl2 = 1;
-    auto rotate = [&] {
-        const int t = sl2;
-        sl2 = sl1;
-        sl1 = sl0;
-        sl0 = t;
-    };
-    // row step y (strip-local input row, window of output row y - 1)
-    for (int y = oy0 - 1; y <= oy1; y++, rotate()) {
-        const int slot = sl0;
+
+    // row step y (strip-local input row, window of output row y - 1) in ring phase PH
+    auto step = [&](const int S0, const int S1, const int S2, const int y) -> unsigned {
         __syncwarp();  // the previous step's readers are done with this slot
         // ---- 1. stage the new pixel ---------------------------------------
         uint32_t r8, g8, b8;
@@ -190,13 +367,13 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
             // shuffle, two whole 16-byte stores (lane 31's second half: unused)
             const float sx = __shfl_down_sync(0xffffffffu, q.x, 1), sy = __shfl_down_sync(0xffffffffu, q.y, 1);
             const float sz = __shfl_down_sync(0xffffffffu, q.z, 1), sa = __shfl_down_sync(0xffffffffu, q.aux, 1);
-            rA[slot * C::LANES_E + C::EOFF + lane] = make_float4(q.x, sx, q.y, sy);
-            rB[slot * C::LANES_E + C::EOFF + lane] = make_float4(q.z, sz, q.aux, sa);
+            rA[S0 * C::LANES_E + C::EOFF + lane] = make_float4(q.x, sx, q.y, sy);
+            rB[S0 * C::LANES_E + C::EOFF + lane] = make_float4(q.z, sz, q.aux, sa);
             if (lane == 0) {  // element 1 = (pad, pixel 0)
-                rA[slot * C::LANES_E + 1] = make_float4(1.f, q.x, 1.f, q.y);
-                rB[slot * C::LANES_E + 1] = make_float4(1.f, q.z, 1.f, q.aux);
+                rA[S0 * C::LANES_E + 1] = make_float4(1.f, q.x, 1.f, q.y);
+                rB[S0 * C::LANES_E + 1] = make_float4(1.f, q.z, 1.f, q.aux);
             }
-            rK[slot * 32 + lane] = r8 | (g8 << 8) | (b8 << 16);
+            rK[S0 * 32 + lane] = r8 | (g8 << 8) | (b8 << 16);
         }
         const bool zr2 = __any_sync(0xffffffffu, zero);
         const bool zchk = C::NEED_L && (zr0 || zr1 || zr2);  // pairs reach two rows up
@@ -220,19 +397,18 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                 if constexpr (BOTH) v = make_float2(a, l);
                 else if constexpr (C::NEED_A) v = a;
                 else v = l;
-                if (k < 7) rE[(slot * 7 + k) * 32 + lane] = v;
+                if (k < 7) rE[(S0 * 7 + k) * 32 + lane] = v;
                 else rE2[(k - 7) * 32 + lane] = v;
             };
             // all partner loads first, then the six independent packed pair
             // evaluations, then the stores: the pair math chains interleave
-            const int rs1 = sl1, rs2 = sl2;
-            const int rsl[5] = {slot, rs1, rs1, rs2, rs2};
-            const int els[5] = {lane, lane, lane + 2, lane, lane + 2};  // lane 0's (l-2, l-1): pads, unused
+            const int rsl[5] = {S0, S1, S1, S2, S2};
+            constexpr int els[5] = {0, 0, 2, 0, 2};  // + lane; lane 0's (l-2, l-1): pads, unused
             Pair2 pp[6];
 #pragma unroll
             for (int t = 0; t < 5; t++) {
-                const ulonglong2 A2 = lds_u2(rA + rsl[t] * C::LANES_E + els[t]);
-                const ulonglong2 B2 = lds_u2(rB + rsl[t] * C::LANES_E + els[t]);
+                const ulonglong2 A2 = lds_u2(rA + rsl[t] * C::LANES_E + els[t] + lane);
+                const ulonglong2 B2 = lds_u2(rB + rsl[t] * C::LANES_E + els[t] + lane);
                 pp[t] = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
             }
             pp[5] = pv;
@@ -260,67 +436,94 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
         __syncwarp();
         // ---- 3. aggregate + select for output row y - 1 ---------------------
         const int oy = y - 1;
-        if (oy < oy0) continue;  // warm-up rows (uniform across the warp)
+        if (oy < oy0) return 0u;  // warm-up rows (uniform across the warp)
         const bool valid = lane >= 1 && lane < 31 && oy < oy1 && col < kp.W;
-        P2 ag[BOTH ? N : 1];
-        DT cen[CEN ? N : 1];  // centre column
-        float aS[BOTH ? 1 : N];
+        // ring entry of the pair {P, Q}, P = (window row t, this lane),
+        // Q = (window row t2, lane + dv): stored at the lower pixel's lane
+        const int SL[3] = {S2, S1, S0};  // window rows 0, 1, 2 = input rows y-2, y-1, y
+        auto ring = [&](int slot, int k, int off) -> DT {
+            return (k < 7) ? rE[(slot * 7 + k) * 32 + lane + off] : rE2[(k - 7) * 32 + lane + off];
+        };
+        auto pairv = [&](int t, int t2, int dv) -> DT {
+            if (t2 > t || (t2 == t && dv > 0)) return ring(SL[t2], w3_k(t2 - t, dv), dv);  // Q lower
+            return ring(SL[t], w3_k(t - t2, -dv), 0);                                      // P lower
+        };
+        using AG = typename std::conditional<BOTH, P2, float>::type;
+        auto toag = [](DT v) -> AG {
+            if constexpr (BOTH) return *reinterpret_cast<const P2 *>(&v);
+            else return v;
+        };
+        auto agadd = [](AG a, AG b) -> AG {
+            if constexpr (BOTH) return add2(a, b);
+            else return a + b;
+        };
+        AG ag[N];
 #pragma unroll
-        for (int i = 0; i < N; i++) {
-            if constexpr (BOTH) ag[i] = pk2(kp.self_term, 0.f);
-            else aS[i] = C::NEED_A ? kp.self_term : 0.f;
+        for (int t = 0; t < 3; t++) {
+            AG V[5];
+#pragma unroll
+            for (int dv = -2; dv <= 2; dv++) {
+                AG acc{};
+                bool first = true;
+#pragma unroll
+                for (int t2 = 0; t2 < 3; t2++) {
+                    if (t2 == t && dv == 0) continue;  // the pixel itself: self term below
+                    const AG x = toag(pairv(t, t2, dv));
+                    acc = first ? x : agadd(acc, x);
+                    first = false;
+                }
+                V[dv + 2] = acc;
+            }
+            if constexpr (ST == ST_MINIMAX && C::NEED_A) {  // the self term (angular only)
+                if constexpr (BOTH) V[2] = add2(V[2], pk2(kp.self_term, 0.f));
+                else V[2] += kp.self_term;
+            }
+            const AG a = agadd(V[2], V[3]);
+            const AG aR = agadd(a, V[4]);                 // window columns +0..+2: output one lane right
+            const AG aC = agadd(a, V[1]);                 // -1..+1: this lane's output
+            const AG aL = agadd(agadd(V[0], V[1]), V[2]);  // -2..0: output one lane left
+            if constexpr (BOTH) {
+                ag[3 * t + 0].v = __shfl_up_sync(0xffffffffu, aR.v, 1);
+                ag[3 * t + 2].v = __shfl_down_sync(0xffffffffu, aL.v, 1);
+            } else {
+                ag[3 * t + 0] = __shfl_up_sync(0xffffffffu, aR, 1);
+                ag[3 * t + 2] = __shfl_down_sync(0xffffffffu, aL, 1);
+            }
+            ag[3 * t + 1] = aC;
         }
+        DT cen[CEN ? N : 1];  // centre column d(i, centre): the centre is (window row 1, this lane)
         if constexpr (CEN) {
-            if constexpr (BOTH) cen[DC] = make_float2(kp.self_term, 0.f);
-            else cen[DC] = 0.f;
-        }
-        const int lc = min(max(lane, 1), 30);  // clamp so lanes 0/31 read in-bounds (results unused)
-        // ring rows of the window's input rows oy-1, oy, oy+1 (slots of y-2, y-1, y)
-        const int s0 = sl2, s1 = sl1, s2 = sl0;
-        const DT *eR[3] = {rE + s0 * 7 * 32 + lc - 1, rE + s1 * 7 * 32 + lc - 1, rE + s2 * 7 * 32 + lc - 1};
-        const DT *eR2 = rE2 + lc - 1;
-        const uint32_t *kR[3] = {rK + s0 * 32 + lc - 1, rK + s1 * 32 + lc - 1, rK + s2 * 32 + lc - 1};
 #pragma unroll
-        for (int j = 1; j < N; j++) {
-#pragma unroll
-            for (int i = 0; i < j; i++) {
-                const int du = j / 3 - i / 3, dv = j % 3 - i % 3;
-                const int k = w3_k(du, dv);
-                // lower pixel j: window row j/3 -> input row oy - 1 + j/3, lane lc - 1 + j%3
-                const DT val = (k < 7) ? eR[j / 3][k * 32 + j % 3] : eR2[(k - 7) * 32 + j % 3];
-                if constexpr (BOTH) {
-                    const P2 x = *reinterpret_cast<const P2 *>(&val);
-                    ag[i] = add2(ag[i], x);
-                    ag[j] = add2(ag[j], x);
-                } else {
-                    aS[i] += val;
-                    aS[j] += val;
-                }
-                if constexpr (CEN) {
-                    if (j == DC) cen[i] = val;
-                    else if (i == DC) cen[j] = val;
-                }
+            for (int i = 0; i < N; i++) {
+                const int u = i / 3, v = i % 3;
+                if (i == DC) {
+                    if constexpr (BOTH) cen[i] = make_float2(kp.self_term, 0.f);
+                    else cen[i] = C::NEED_A ? kp.self_term : 0.f;
+                } else if (u == 0) cen[i] = ring(S1, w3_k(1, 1 - v), 0);  // centre lower
+                else if (u == 1) cen[i] = v == 0 ? ring(S1, w3_k(0, 1), 0) : ring(S1, w3_k(0, 1), 1);
+                else cen[i] = ring(S0, w3_k(1, v - 1), v - 1);            // pixel i lower
             }
         }
         // colours of the window (rings hold input rows oy-1, oy, oy+1)
+        const int lc = min(max(lane, 1), 30);  // clamp so lanes 0/31 read in-bounds (results unused)
         uint32_t wc[N];
 #pragma unroll
-        for (int i = 0; i < N; i++) wc[i] = kR[i / 3][i % 3];
+        for (int i = 0; i < N; i++) wc[i] = rK[SL[i / 3] * 32 + lc - 1 + i % 3];
         uint32_t cb;
         bool doubt;
         {
-            auto col = [&](auto ic) { return wc[decltype(ic)::value]; };
+            auto colf = [&](auto ic) { return wc[decltype(ic)::value]; };
             if constexpr (BOTH) {
                 auto A = [&](auto ic) { return lo2(ag[decltype(ic)::value]); };
                 auto L = [&](auto ic) { return hi2(ag[decltype(ic)::value]); };
                 auto AD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value].x; else return 0.f; };
                 auto LD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value].y; else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, cb, doubt);
+                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, colf, cb, doubt);
             } else {
-                auto V = [&](auto ic) { return aS[decltype(ic)::value]; };
+                auto V = [&](auto ic) { return ag[decltype(ic)::value]; };
                 auto Z = [](auto) { return 0.f; };
                 auto CD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value]; else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, col, cb, doubt);
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, colf, cb, doubt);
             }
         }
         uint8_t *orow = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch;
@@ -332,56 +535,48 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                     d[i] = lo2(ag[i]);
                     d[N + i] = hi2(ag[i]);
                 } else {
-                    d[i] = C::NEED_A ? aS[i] : 0.f;
-                    d[N + i] = C::NEED_L ? aS[i] : 0.f;
+                    d[i] = C::NEED_A ? ag[i] : 0.f;
+                    d[N + i] = C::NEED_L ? ag[i] : 0.f;
                 }
             }
         }
-        if (valid) {
+        // ---- 4. doubtful pixels: queued for the drain, or re-decided inline
+        // by the caller (one call site) ----------------------------------------
+        unsigned mask = __ballot_sync(0xffffffffu, valid && doubt && !kp.diag_no_fixup);
+        bool queued = false;
+        if (!HIO && mask && kp.w3_queue) {
+            unsigned base = 0;
+            if (lane == 0) {
+                base = atomicAdd(kp.flag_count + kQueueWord, (unsigned)__popc(mask));
+                atomicAdd(kp.flag_count, (unsigned)__popc(mask));
+            }
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if ((mask >> lane) & 1u) {
+                const unsigned idx = base + __popc(mask & ((1u << lane) - 1u));
+                if (idx < (unsigned)kp.w3_queue) {
+                    uint4 *qe = w3_queue_entries(kp) + idx;
+                    qe->x = (unsigned)frame;
+                    qe->y = (unsigned)oy;
+                    qe->z = (unsigned)col;
+                    __threadfence();
+                    // publish; a drainer that raced ahead left it abandoned
+                    // (2): then this lane's pixel is re-decided inline
+                    if (atomicCAS(&qe->w, 0u, 1u) == 0u) queued = true;
+                    else qe->w = 0u;
+                }
+            }
+            mask &= ~__ballot_sync(0xffffffffu, queued);  // queue overflow: re-decided inline
+            if (mask && lane == 0) atomicAdd(kp.flag_count, 0u - (unsigned)__popc(mask));  // counted inline
+        }
+        if (valid && !queued) {
             uint8_t *op = HIO ? ostage + 3 * (lane - 1) : orow + col * 3;
             op[0] = (uint8_t)(cb & 0xff);
             op[1] = (uint8_t)((cb >> 8) & 0xff);
             op[2] = (uint8_t)((cb >> 16) & 0xff);
         }
-        // ---- 4. float64 re-decision of doubtful pixels (whole warp) -------
-        unsigned mask = __ballot_sync(0xffffffffu, valid && doubt && !kp.diag_no_fixup);
-        if (mask) {
-            if (lane == 0) atomicAdd(kp.flag_count, (unsigned)__popc(mask));
-            E64 *e64 = reinterpret_cast<E64 *>(f64b);
-            double *dA = reinterpret_cast<double *>(e64 + N);
-            double *dL = dA + 36;
-            while (mask) {
-                const int fl = __ffs(mask) - 1;
-                mask &= mask - 1;
-                if (lane < N) {
-                    const int i = lane;
-                    const int sr = i < 3 ? sl2 : (i < 6 ? sl1 : sl0);
-                    const uint32_t cc = rK[sr * 32 + fl - 1 + i % 3];
-                    prep64(make_float4((float)(cc & 0xff), (float)((cc >> 8) & 0xff), (float)((cc >> 16) & 0xff), 0.f),
-                           ST, e64[i]);
-                }
-                __syncwarp();
-                pair_tables<false>(e64, kp.fp, lane, 32, dA, dL, C::NEED_A, C::NEED_L);
-                __syncwarp();
-                double m;
-                int bb = decide64(e64, kp.fp, lane, dA, dL, &m);
-                if (ST == ST_EXACT && C::NEED_A && m < kp.fp.cr_margin) {
-                    if (lane == 0) atomicAdd(kp.flag_count + 1, 1u);
-                    __syncwarp();
-                    pair_tables<true>(e64, kp.fp, lane, 32, dA, dL, C::NEED_A, C::NEED_L);
-                    __syncwarp();
-                    bb = decide64(e64, kp.fp, lane, dA, dL, &m);
-                }
-                if (lane == 0) {
-                    uint8_t *op = HIO ? ostage + 3 * (fl - 1) : orow + (strip * 30 - 1 + fl) * 3;
-                    op[0] = (uint8_t)e64[bb].raw[0];
-                    op[1] = (uint8_t)e64[bb].raw[1];
-                    op[2] = (uint8_t)e64[bb].raw[2];
-                }
-                __syncwarp();
-            }
-        }
-        if constexpr (HIO) {  // the staged row segment -> host as aligned words
+        if constexpr (HIO) {
+            if (mask) w3_redecide<FAM, ST>(kp, rK, S0, S1, S2, f64b, mask, ostage);
+            // the staged row segment -> host as aligned words
             __syncwarp();
             const int nv = min(30, kp.W - strip * 30);
             if (oy < oy1 && nv > 0) {
@@ -401,7 +596,27 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const K
                     }
                 }
             }
+            return 0u;
+        } else {
+            return mask;
         }
+    };
+    int s0 = 0, s1 = 2, s2 = 1;  // ring slots of rows y, y-1, y-2 (rotated each step)
+    for (int y = oy0 - 1; y <= oy1; y++) {
+        const unsigned mask = step(s0, s1, s2, y);
+        if (mask) {
+            uint8_t *orow = out + (long long)frame * kp.out_fstride + (long long)(y - 1) * kp.out_pitch;
+            w3_redecide<FAM, ST>(kp, rK, s0, s1, s2, f64b, mask, orow + strip * 30 * 3);
+        }
+        const int t = s2;
+        s2 = s1;
+        s1 = s0;
+        s0 = t;
+    }
+    if (!HIO && kp.w3_queue) {
+        const int per_frame = n_strips * n_chunks;
+        const unsigned cta_warps = (unsigned)min(C::WARPS, per_frame - (int)blockIdx.x * C::WARPS);
+        w3_drain<FAM, ST>(kp, in, out, f64b, cta_warps, gridDim.x * gridDim.z, &s_done);
     }
 }
 
@@ -409,8 +624,9 @@ template <int FAM, int ST, int PC>
 cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp)
 {
     using C = W3Cfg<FAM>;
-    auto kern = kp.hostio ? dfg_w3_kernel<FAM, ST, PC, true> : dfg_w3_kernel<FAM, ST, PC, false>;
-    static unsigned long long configured[2] = {0, 0};
+    constexpr int minb = w3_minb<ST>();
+    auto kern = kp.hostio ? dfg_w3_kernel<FAM, ST, PC, true, minb> : dfg_w3_kernel<FAM, ST, PC, false, minb>;
+    static unsigned long long configured[2] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(configured[kp.hostio] & (1ull << (dev & 63)))) {
@@ -430,7 +646,7 @@ cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KP
         const char *e = getenv("DFG_W3_RPC");  // diagnostics only
         return e ? atoi(e) : 0;
     }();
-    const long long wps = env_wps > 0 ? env_wps : 16;
+    const long long wps = env_wps > 0 ? env_wps : 2 * minb;
     const long long slots = 148 * wps;
     const long long cols = (long long)n_strips * kp.n_frames;  // independent strip columns
     const long long strip_rows = cols * kp.out_rows;

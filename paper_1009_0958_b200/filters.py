@@ -104,15 +104,19 @@ def _validate_spec(spec) -> None:
             raise ValueError(f"lambda {spec.acwddf.lam} too large for a window of {n} vectors")
 
 
-def workspace(nbytes: int, device=None):
-    """A cached device workspace of at least ``nbytes`` for ``device``."""
+def workspace(nbytes: int, device=None, stream=None):
+    """A cached, zeroed device workspace of at least ``nbytes`` for
+    ``device``, one per stream: a workspace serves one call at a time (it
+    holds the row sweep's re-decision queue), and calls on one stream are
+    ordered."""
     torch = _torch()
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
+    key = (dev.index, _stream_ptr(torch, stream, dev).value)
     with _ws_lock:
-        buf = _ws_cache.get(dev.index)
+        buf = _ws_cache.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
-            _ws_cache[dev.index] = buf
+            _ws_cache[key] = buf
         return buf
 
 
@@ -137,7 +141,7 @@ def filter_device(x, spec, policy=REPLICATE, out=None, stream=None, ws=None):
     prm = _params(spec, policy)
     need = _lib.lib().dfg_workspace_bytes(H * W)
     if ws is None:
-        ws = workspace(need, x.device)
+        ws = workspace(need, x.device, stream)
     with _on_device(torch, x.device):
         rc = _lib.lib().dfg_filter(ctypes.c_void_p(x.data_ptr()), H, W, x.stride(0),
                                    ctypes.c_void_p(out.data_ptr()), out.stride(0), ctypes.byref(prm),
@@ -160,7 +164,7 @@ def filter_batch_device(x, spec, policy=REPLICATE, out=None, stream=None, ws=Non
     prm = _params(spec, policy)
     need = _lib.lib().dfg_workspace_bytes(B * H * W)
     if ws is None:
-        ws = workspace(need, x.device)
+        ws = workspace(need, x.device, stream)
     with _on_device(torch, x.device):
         rc = _lib.lib().dfg_filter_batch(ctypes.c_void_p(x.data_ptr()), B, H, W, x.stride(1), x.stride(0),
                                          ctypes.c_void_p(out.data_ptr()), out.stride(1), out.stride(0),
@@ -185,7 +189,7 @@ def filter_rows_device(x, global_H, in_row0, out_row0, out_rows, spec, policy=RE
     prm = _params(spec, policy)
     need = _lib.lib().dfg_workspace_bytes(out_rows * W)
     if ws is None:
-        ws = workspace(need, x.device)
+        ws = workspace(need, x.device, stream)
     with _on_device(torch, x.device):
         rc = _lib.lib().dfg_filter_rows(ctypes.c_void_p(x.data_ptr()), int(global_H), W, int(in_row0), in_rows,
                                         x.stride(0), ctypes.c_void_p(out.data_ptr()), int(out_row0),
