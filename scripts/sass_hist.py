@@ -20,6 +20,7 @@ div = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 print(f"total warp instructions {tot} ({tot/div:.1f} per unit)")
 for op, n in h.most_common(45):
     print(f"{n/div:9.1f} {100*n/tot:5.1f}%  stall {st[op]:6d}  {op}")
+print("=== per instruction")
 if len(sys.argv) > 3:
     for a, s, n, smp in seq:
         if n/div >= float(sys.argv[3]): print(f"{n/div:7.2f} {smp:5d} {s}")
