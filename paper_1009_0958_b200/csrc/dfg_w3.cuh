@@ -355,12 +355,16 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
             b8 = nb8;
             if (y < oy1) load_px(y + 1, nr8, ng8, nb8);
         }
-        const bool zero = (r8 | g8 | b8) == 0;
+        const uint32_t rgb = r8 | (g8 << 8) | (b8 << 16);
+        const bool zero = rgb == 0u;
+        // gray map: the zero vector -> (1, 1, 1) (its channels are 0, so OR-ing
+        // the flag in maps exactly it); exact u8 -> float without I2F: 2^23 + v,
+        // minus 2^23
+        const uint32_t zf = zero ? 1u : 0u;
         Pix q;
-        // exact u8 -> float without I2F: 2^23 + v, minus 2^23
-        q.x = zero ? 1.f : __uint_as_float(0x4B000000u | r8) - 8388608.f;
-        q.y = zero ? 1.f : __uint_as_float(0x4B000000u | g8) - 8388608.f;
-        q.z = zero ? 1.f : __uint_as_float(0x4B000000u | b8) - 8388608.f;
+        q.x = __uint_as_float(0x4B000000u | r8 | zf) - 8388608.f;
+        q.y = __uint_as_float(0x4B000000u | g8 | zf) - 8388608.f;
+        q.z = __uint_as_float(0x4B000000u | b8 | zf) - 8388608.f;
         q.aux = encode_aux<ST, C::NEED_L>(q.x, q.y, q.z, zero);
         {
             // element l = pixel pair (l, l+1): the right neighbour's record by
@@ -373,7 +377,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
                 rA[S0 * C::LANES_E + 1] = make_float4(1.f, q.x, 1.f, q.y);
                 rB[S0 * C::LANES_E + 1] = make_float4(1.f, q.z, 1.f, q.aux);
             }
-            rK[S0 * 32 + lane] = r8 | (g8 << 8) | (b8 << 16);
+            rK[S0 * 32 + lane] = rgb;
         }
         const bool zr2 = __any_sync(0xffffffffu, zero);
         const bool zchk = C::NEED_L && (zr0 || zr1 || zr2);  // pairs reach two rows up
