@@ -13,6 +13,7 @@ from .filters import (
     filter_batch_device,
     filter_device,
     filter_host,
+    filter_host_frames,
     filter_rows_device,
     fixup_counts,
     last_fixup_count,
@@ -45,7 +46,7 @@ __all__ = [
     "CALIBRATION_INTERCEPT", "CALIBRATION_SLOPE", "ColorVector", "DirectionalStrategy",
     "FAMILIES", "FastAcosTable", "FilterSpec", "MinimaxPoly", "REFLECT", "REPLICATE",
     "RasterImage", "apply_filter", "center_weight", "filter_batch_device", "filter_device",
-    "filter_host", "filter_rows_device", "fixup_counts", "last_fixup_count", "parse_filter_spec", "to_uint8",
+    "filter_host", "filter_host_frames", "filter_rows_device", "fixup_counts", "last_fixup_count", "parse_filter_spec", "to_uint8",
     "MetricsReport", "compare", "mae", "psnr", "ncd", "metrics_device",
     "NoiseParams", "corrupt_device", "corrupt_image",
     "LinearFit", "fit_angular_chromaticity", "fit_line", "sample_angle_chromaticity_pairs",

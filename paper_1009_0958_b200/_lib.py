@@ -19,7 +19,7 @@ BORDER_CODE = {"replicate": 0, "reflect": 1}
 # every symbol include/dirfilt_gpu.h declares
 EXPORTS = (
     "dfg_abi_version", "dfg_last_error", "dfg_workspace_bytes", "dfg_filter",
-    "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_fixup_count",
+    "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_filter_host_frames", "dfg_fixup_count",
     "dfg_reset_counts", "dfg_debug_values", "dfg_cr_acos_host", "dfg_corrupt_image",
     "dfg_image_metrics", "dfg_calib_scratch_bytes", "dfg_calib_reduce", "dfg_calib_samples",
 )
@@ -90,6 +90,7 @@ def lib() -> ctypes.CDLL:
     L.dfg_filter_rows.argtypes = [vp, i32, i32, i32, i32, i64, vp, i32, i32, i64, P, vp, sz, vp]
     L.dfg_filter_batch.argtypes = [vp, i32, i32, i32, i64, i64, vp, i64, i64, P, vp, sz, vp]
     L.dfg_filter_host.argtypes = [vp, i32, i32, vp, P, vp]
+    L.dfg_filter_host_frames.argtypes = [vp, vp, i32, i32, i32, P, vp]
     L.dfg_fixup_count.argtypes = [vp, vp, ctypes.POINTER(i64)]
     L.dfg_reset_counts.argtypes = [vp, vp]
     L.dfg_debug_values.argtypes = [vp, i32, i32, i64, vp, P, vp]
@@ -101,7 +102,7 @@ def lib() -> ctypes.CDLL:
     L.dfg_calib_reduce.argtypes = [ctypes.POINTER(DfgCalibParams), i32, ctypes.c_double, ctypes.c_double,
                                    ctypes.POINTER(ctypes.c_double), vp, sz, vp]
     L.dfg_calib_samples.argtypes = [ctypes.POINTER(DfgCalibParams), vp, vp, vp]
-    for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host",
+    for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_filter_host_frames",
                  "dfg_fixup_count", "dfg_reset_counts", "dfg_debug_values", "dfg_corrupt_image",
                  "dfg_image_metrics", "dfg_calib_reduce", "dfg_calib_samples"):
         getattr(L, name).restype = ctypes.c_int

@@ -530,6 +530,107 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
     return DFG_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Frame stream from host memory: kFrameSlots device slots, each with its own
+// input/output buffers, workspace and stream.  Frame f goes to slot f % S:
+// H2D, kernel, D2H in that slot's stream, so frame f's H2D overlaps frame
+// f-1's kernel and frame f-2's D2H (PCIe is full duplex and the SMs are idle
+// during the copies); a slot is reused only after its previous frame's D2H.
+constexpr int kFrameSlots = 3;
+
+struct FrameCache {
+    uint8_t *d_in[kFrameSlots] = {}, *d_out[kFrameSlots] = {};
+    void *ws[kFrameSlots] = {};
+    cudaStream_t s[kFrameSlots] = {};
+    cudaEvent_t ev_start = nullptr, ev_end[kFrameSlots] = {};
+    size_t px_cap = 0;
+    int dev = -1;
+    void release()
+    {
+        for (int k = 0; k < kFrameSlots; k++) {
+            if (d_in[k]) cudaFree(d_in[k]);
+            if (d_out[k]) cudaFree(d_out[k]);
+            if (ws[k]) cudaFree(ws[k]);
+            d_in[k] = d_out[k] = nullptr;
+            ws[k] = nullptr;
+        }
+        px_cap = 0;
+    }
+    ~FrameCache() { release(); }
+};
+thread_local FrameCache g_frames;
+
+}  // namespace
+
+extern "C" {
+
+int dfg_filter_host_frames(const uint8_t *const *h_in, uint8_t *const *h_out, int32_t n_frames, int32_t H,
+                           int32_t W, const dfg_params *prm, void *stream)
+{
+    int rc = validate(prm);
+    if (rc) return rc;
+    if (n_frames < 0) return fail(DFG_E_ARG, "negative frame count");
+    if (H < 1 || W < 1) return fail(DFG_E_ARG, "image must contain at least one pixel");
+    if (n_frames == 0) return DFG_OK;
+    if (!h_in || !h_out) return fail(DFG_E_ARG, "null frame list");
+    for (int f = 0; f < n_frames; f++)
+        if (!h_in[f] || !h_out[f]) return fail(DFG_E_ARG, "null host frame pointer");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    FrameCache &c = g_frames;
+    const size_t px = (size_t)H * W, nbytes = 3 * px;
+    const size_t wsb = dfg_workspace_bytes((int64_t)px);
+    cudaError_t e = cudaSuccess;
+    if (c.dev != dev || c.px_cap < px) {
+        c.release();
+        for (int k = 0; k < kFrameSlots && e == cudaSuccess; k++) {
+            e = cudaMalloc(&c.d_in[k], nbytes);
+            if (e == cudaSuccess) e = cudaMalloc(&c.d_out[k], nbytes);
+            if (e == cudaSuccess) e = cudaMalloc(&c.ws[k], wsb);
+            if (e == cudaSuccess) e = cudaMemset(c.ws[k], 0, wsb);
+        }
+        if (e == cudaSuccess && c.dev != dev) {
+            e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
+            for (int k = 0; k < kFrameSlots && e == cudaSuccess; k++) {
+                e = cudaStreamCreateWithFlags(&c.s[k], cudaStreamNonBlocking);
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_end[k], cudaEventDisableTiming);
+            }
+        }
+        if (e != cudaSuccess) {
+            c.release();
+            return cuda_fail(e, "frame slot allocation");
+        }
+        c.px_cap = px;
+        c.dev = dev;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    // fork: the slots start after prior work on `st`
+    e = cudaEventRecord(c.ev_start, st);
+    for (int k = 0; k < kFrameSlots && e == cudaSuccess; k++) e = cudaStreamWaitEvent(c.s[k], c.ev_start, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "fork");
+    const long long pitch = 3LL * W;
+    for (int f = 0; f < n_frames; f++) {
+        const int k = f % kFrameSlots;
+        e = cudaMemcpyAsync(c.d_in[k], h_in[f], nbytes, cudaMemcpyHostToDevice, c.s[k]);
+        if (e != cudaSuccess) return cuda_fail(e, "frame H2D");
+        rc = run(c.d_in[k], H, W, 0, H, pitch, 0, c.d_out[k], 0, H, pitch, 0, 1, prm, c.ws[k], wsb, c.s[k], nullptr);
+        if (rc) return rc;
+        e = cudaMemcpyAsync(h_out[f], c.d_out[k], nbytes, cudaMemcpyDeviceToHost, c.s[k]);
+        if (e != cudaSuccess) return cuda_fail(e, "frame D2H");
+    }
+    // join, then wait for the whole stream of frames
+    for (int k = 0; k < kFrameSlots && e == cudaSuccess; k++) {
+        e = cudaEventRecord(c.ev_end[k], c.s[k]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_end[k], 0);
+    }
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(e, "frame stream synchronize");
+    return DFG_OK;
+}
+
 int dfg_fixup_count(const void *ws, void *stream, int64_t *count)
 {
     if (!ws || !count) return fail(DFG_E_ARG, "null argument");

@@ -222,6 +222,41 @@ def filter_host(pixels_u8: np.ndarray, spec, policy=REPLICATE, out: np.ndarray |
     return out
 
 
+def filter_host_frames(frames, spec, policy=REPLICATE, out=None, stream=None):
+    """A stream of independent host frames through ``dfg_filter_host_frames``:
+    ``frames`` is a sequence of C-contiguous uint8 (H, W, 3) arrays of one
+    shape (or an (F, H, W, 3) array); returns the list of filtered frames
+    (written into ``out``'s arrays when given).  Up to three frames are in
+    flight, so frame f's copy to the device overlaps frame f-1's kernel and
+    frame f-2's copy back; pin the buffers for the overlap.  Each output
+    equals ``filter_host`` of its frame."""
+    torch = _torch()
+    prm = _params(spec, policy)
+    ins = [f for f in frames]
+    if not ins:
+        return []
+    shape = ins[0].shape
+    if len(shape) != 3 or shape[2] != 3:
+        raise ValueError(f"pixel arrays must have shape (M, N, 3), got {shape}")
+    for a in ins:
+        if (type(a) is not np.ndarray or a.dtype != np.uint8 or not a.flags.c_contiguous or a.shape != shape):
+            raise ValueError("frames must be C-contiguous uint8 arrays of one (M, N, 3) shape")
+    if out is None:
+        out = [np.empty_like(a) for a in ins]
+    else:
+        out = [o for o in out]
+        if len(out) != len(ins) or any(type(o) is not np.ndarray or o.dtype != np.uint8 or o.shape != shape or
+                                       not o.flags.c_contiguous or not o.flags.writeable for o in out):
+            raise ValueError("out must hold one writable C-contiguous uint8 array per frame, of the frames' shape")
+    n = len(ins)
+    pin = (ctypes.c_void_p * n)(*[a.ctypes.data for a in ins])
+    pout = (ctypes.c_void_p * n)(*[o.ctypes.data for o in out])
+    rc = _lib.lib().dfg_filter_host_frames(pin, pout, n, shape[0], shape[1], ctypes.byref(prm),
+                                           _stream_ptr(torch, stream, None))
+    _lib.check(rc)
+    return out
+
+
 def fixup_counts(device=None, stream=None, reset: bool = False):
     """(pixels re-decided in float64, of which needed the correctly rounded
     arccos pass) accumulated on ``device``'s cached workspace since the last

@@ -237,3 +237,25 @@ def test_host_streaming_3x3_against_oracle(cuda, spec, mode, monkeypatch):
         assert (got == want).all(), (spec, H, W, border, int((got != want).any(-1).sum()))
         guard = buf_out.numpy()
         assert (guard[:3 - shift] == 7).all() and (guard[3 - shift + n:] == 7).all()  # no stray writes
+
+
+@pytest.mark.parametrize("spec", ["ddf:exact", "acwddf:minimax:window=5", "bvdf:rgb:window=7"])
+def test_host_frame_stream(cuda, spec):
+    """dfg_filter_host_frames: frames round-robin over three device slots
+    (copies of frame f overlap the kernels of its neighbours); every frame
+    must equal the oracle, for pinned and pageable buffers and frame counts
+    below, at and above the slot count."""
+    torch = cuda
+    from paper_1009_0958_b200 import filter_host_frames
+    s = parse_filter_spec(spec)
+    for n, pinned in ((1, True), (3, False), (7, True)):
+        imgs = [synth.noisy_image(75, 64, 30 + i, ("correlated", 0.2)) for i in range(n)]
+        if pinned:
+            ins = [torch.from_numpy(a).pin_memory().numpy() for a in imgs]
+            outs = [torch.empty(a.shape, dtype=torch.uint8).pin_memory().numpy() for a in imgs]
+        else:
+            ins, outs = imgs, None
+        got = filter_host_frames(ins, s, out=outs)
+        for a, g in zip(imgs, got):
+            assert (g == oracle.filter_image(a, s)).all(), (spec, n, pinned)
+    assert filter_host_frames([], s) == []
