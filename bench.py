@@ -380,6 +380,12 @@ def run_ours(args, config):
     _lib.check(_lib.lib().dfg_fixup_count(ctypes.c_void_p(ws_buf.data_ptr()), None, ctypes.byref(cnt)))
     redecided = int(cnt.value)
 
+    # launch cover: a ~40 us device-side sleep between the L2 flush and each
+    # start event, so the host's Python/ctypes launch path (tens of us) runs
+    # while the GPU is still busy and the events bracket the kernel itself,
+    # not the host launch latency (the role the SURVEY 8(d) graph capture of
+    # C1/C2 plays; a graph cannot interleave the per-step L2 flush)
+    cover_cycles = 0 if os.environ.get("BENCH_NO_COVER") else 80000
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
@@ -388,6 +394,8 @@ def run_ours(args, config):
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.fill_(k & 0xff)
+            if cover_cycles:
+                torch.cuda._sleep(cover_cycles)  # the step's launch is queued before its start event fires
             starts[k].record()
             step()
             ends[k].record()
@@ -458,7 +466,7 @@ def run_ours(args, config):
         "data": "synthetic (seeded gradient + 20 rectangles + impulsive noise, SURVEY 8(d))",
         "config": {"workload": config, "spec": cfg["spec"], "shape": list(cfg["shape"]),
                    "noise": list(cfg["noise"]), "seed": cfg["seed"], "frames": cfg.get("frames", 1),
-                   "l2": "flushed between timed steps (256 MiB write)", "parallelism": f"{wl['kind']} x{world}"},
+                   "l2": "flushed between timed steps (256 MiB write)", "launch": ("host launch hidden behind a device sleep before each start event" if not os.environ.get("BENCH_NO_COVER") else "uncovered"), "parallelism": f"{wl['kind']} x{world}"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "redecided_px_per_step": redecided, "clocks": clk.summary(),
         **({"quality": quality} if quality else {}),
