@@ -529,33 +529,95 @@ struct Pick {
 // exact-zero winner exactly -- the first index wins in both -- and are not
 // counted as competitors.  (A near-zero FP32 value the reference may round to
 // 0 stays a competitor: the absolute bound flags it.)
+// Tournament form of the window-order scan: each merge of two adjacent
+// index ranges keeps the left (lower-index) winner unless the right one is
+// strictly smaller, so the root is the first strict minimum -- the same
+// result as the sequential scan (E:317-355) with log2(N) instead of N - 1
+// dependent compare/select steps (same instruction count).
+template <int LO, int HI, bool PAY, typename FV, typename FC, typename FA, typename FL>
+__device__ __forceinline__ Pick pick_range(FV &val, FC &col, FA &pa, FL &pl)
+{
+    if constexpr (HI - LO == 1) {
+        Pick r;
+        r.v1 = val(std::integral_constant<int, LO>{});
+        r.i1 = LO;
+        r.k1 = col(std::integral_constant<int, LO>{});
+        if constexpr (PAY) {
+            r.xa = pa(std::integral_constant<int, LO>{});
+            r.xl = pl(std::integral_constant<int, LO>{});
+        }
+        return r;
+    } else {
+        constexpr int MID = LO + (HI - LO + 1) / 2;
+        Pick a = pick_range<LO, MID, PAY>(val, col, pa, pl);
+        const Pick b = pick_range<MID, HI, PAY>(val, col, pa, pl);
+        const bool p = b.v1 < a.v1;
+        a.v1 = p ? b.v1 : a.v1;
+        a.i1 = p ? b.i1 : a.i1;
+        a.k1 = p ? b.k1 : a.k1;
+        if constexpr (PAY) {
+            a.xa = p ? b.xa : a.xa;
+            a.xl = p ? b.xl : a.xl;
+        }
+        return a;
+    }
+}
+
+// min (or max) over f(I), I in [LO, HI), as a balanced tree (exact: min and
+// max do not round, so any order gives the same value)
+template <int LO, int HI, bool MAX, typename F>
+__device__ __forceinline__ float tree_minmax(F &f)
+{
+    if constexpr (HI - LO == 1) {
+        return f(std::integral_constant<int, LO>{});
+    } else {
+        constexpr int MID = LO + (HI - LO + 1) / 2;
+        const float a = tree_minmax<LO, MID, MAX>(f), b = tree_minmax<MID, HI, MAX>(f);
+        return MAX ? fmaxf(a, b) : fminf(a, b);
+    }
+}
+
+// (7x7 keeps the sequential scan: the tree's wider live set spills there)
 template <int N, bool PAY, bool ZX, typename FV, typename FC, typename FA, typename FL>
 __device__ __forceinline__ Pick pick(FV val, FC col, FA pa, FL pl)
 {
+    constexpr bool TREE = N <= 25;
     Pick r;
-    r.v1 = val(std::integral_constant<int, 0>{});
-    r.i1 = 0;
-    r.k1 = col(std::integral_constant<int, 0>{});
-    if constexpr (PAY) {
-        r.xa = pa(std::integral_constant<int, 0>{});
-        r.xl = pl(std::integral_constant<int, 0>{});
-    }
-    static_for<1, N>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
-        const float v = val(ic);
-        const bool p = v < r.v1;
-        r.v1 = p ? v : r.v1;
-        r.i1 = p ? i : r.i1;
-        r.k1 = p ? col(ic) : r.k1;
+    if constexpr (TREE) {
+        r = pick_range<0, N, PAY>(val, col, pa, pl);
+    } else {
+        r.v1 = val(std::integral_constant<int, 0>{});
+        r.i1 = 0;
+        r.k1 = col(std::integral_constant<int, 0>{});
         if constexpr (PAY) {
-            r.xa = p ? pa(ic) : r.xa;
-            r.xl = p ? pl(ic) : r.xl;
+            r.xa = pa(std::integral_constant<int, 0>{});
+            r.xl = pl(std::integral_constant<int, 0>{});
         }
-    });
-    r.other = __int_as_float(0x7f800000);
-    static_for<0, N>([&](auto ic) {
-        if (col(ic) != r.k1 && (!ZX || val(ic) > 0.f)) r.other = fminf(r.other, val(ic));
-    });
+        static_for<1, N>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            const float v = val(ic);
+            const bool p = v < r.v1;
+            r.v1 = p ? v : r.v1;
+            r.i1 = p ? i : r.i1;
+            r.k1 = p ? col(ic) : r.k1;
+            if constexpr (PAY) {
+                r.xa = p ? pa(ic) : r.xa;
+                r.xl = p ? pl(ic) : r.xl;
+            }
+        });
+    }
+    const uint32_t k1 = r.k1;
+    if constexpr (TREE) {
+        auto masked = [&](auto ic) {
+            return (col(ic) != k1 && (!ZX || val(ic) > 0.f)) ? val(ic) : __int_as_float(0x7f800000);
+        };
+        r.other = tree_minmax<0, N, false>(masked);
+    } else {
+        r.other = __int_as_float(0x7f800000);
+        static_for<0, N>([&](auto ic) {
+            if (col(ic) != k1 && (!ZX || val(ic) > 0.f)) r.other = fminf(r.other, val(ic));
+        });
+    }
     return r;
 }
 
@@ -572,8 +634,11 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
     auto none = [](auto) { return 0.f; };
     if constexpr (FAM == FAM_ACWDDF) {
         const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
-        float lmax = 0.f;  // largest Minkowski factor of any product (w0 >= w1 >= w2 >= 0)
-        static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, fmaf(w0, LD(ic), L(ic))); });
+        // largest Minkowski factor of any product (w0 >= w1 >= w2 >= 0)
+        auto lf = [&](auto ic) { return fmaf(w0, LD(ic), L(ic)); };
+        float lmax = 0.f;
+        if constexpr (N <= 25) lmax = fmaxf(tree_minmax<0, N, true>(lf), 0.f);
+        else static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, lf(ic)); });
         const Pick sd = pick<N, false, ZX>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
         const Pick s0 = pick<N, true, ZX>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
                                       col, AD, LD);
@@ -601,8 +666,10 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
     } else if constexpr (FAM == FAM_CWDDF) {
         // filters.py:296-328: argmin (A + w AD)(L + w LD), w = n - 2k + 1
         const float w0 = kp.w[0];
+        auto lf = [&](auto ic) { return fmaf(w0, LD(ic), L(ic)); };
         float lmax = 0.f;
-        static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, fmaf(w0, LD(ic), L(ic))); });
+        if constexpr (N <= 25) lmax = fmaxf(tree_minmax<0, N, true>(lf), 0.f);
+        else static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, lf(ic)); });
         const Pick s = pick<N, false, ZX>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
                                       col, none, none);
         kc = s.k1;
@@ -615,7 +682,8 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
         doubt = s.doubtful(er, 0.f);
     } else if constexpr (FAM == FAM_DDF) {
         float lmax = 0.f;
-        static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, L(ic)); });
+        if constexpr (N <= 25) lmax = fmaxf(tree_minmax<0, N, true>(L), 0.f);
+        else static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, L(ic)); });
         const Pick s = pick<N, false, ZX>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
         kc = s.k1;
         doubt = s.doubtful(2.f * er, 2.f * ea * lmax);
