@@ -534,10 +534,13 @@ struct Pick {
 // strictly smaller, so the root is the first strict minimum -- the same
 // result as the sequential scan (E:317-355) with log2(N) instead of N - 1
 // dependent compare/select steps (same instruction count).
-template <int LO, int HI, bool PAY, typename FV, typename FC, typename FA, typename FL>
+// Ranges of at most LEAF candidates are scanned sequentially (7x7 keeps the
+// plain scan: a full tree's wider live set spills there, and four quarter
+// scans merged by the tree measured no faster).
+template <int LO, int HI, int LEAF, bool PAY, typename FV, typename FC, typename FA, typename FL>
 __device__ __forceinline__ Pick pick_range(FV &val, FC &col, FA &pa, FL &pl)
 {
-    if constexpr (HI - LO == 1) {
+    if constexpr (HI - LO <= LEAF) {
         Pick r;
         r.v1 = val(std::integral_constant<int, LO>{});
         r.i1 = LO;
@@ -546,11 +549,23 @@ __device__ __forceinline__ Pick pick_range(FV &val, FC &col, FA &pa, FL &pl)
             r.xa = pa(std::integral_constant<int, LO>{});
             r.xl = pl(std::integral_constant<int, LO>{});
         }
+        static_for<LO + 1, HI>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            const float v = val(ic);
+            const bool p = v < r.v1;
+            r.v1 = p ? v : r.v1;
+            r.i1 = p ? i : r.i1;
+            r.k1 = p ? col(ic) : r.k1;
+            if constexpr (PAY) {
+                r.xa = p ? pa(ic) : r.xa;
+                r.xl = p ? pl(ic) : r.xl;
+            }
+        });
         return r;
     } else {
         constexpr int MID = LO + (HI - LO + 1) / 2;
-        Pick a = pick_range<LO, MID, PAY>(val, col, pa, pl);
-        const Pick b = pick_range<MID, HI, PAY>(val, col, pa, pl);
+        Pick a = pick_range<LO, MID, LEAF, PAY>(val, col, pa, pl);
+        const Pick b = pick_range<MID, HI, LEAF, PAY>(val, col, pa, pl);
         const bool p = b.v1 < a.v1;
         a.v1 = p ? b.v1 : a.v1;
         a.i1 = p ? b.i1 : a.i1;
@@ -565,59 +580,30 @@ __device__ __forceinline__ Pick pick_range(FV &val, FC &col, FA &pa, FL &pl)
 
 // min (or max) over f(I), I in [LO, HI), as a balanced tree (exact: min and
 // max do not round, so any order gives the same value)
-template <int LO, int HI, bool MAX, typename F>
+template <int LO, int HI, bool MAX, int LEAF = 1, typename F>
 __device__ __forceinline__ float tree_minmax(F &f)
 {
-    if constexpr (HI - LO == 1) {
-        return f(std::integral_constant<int, LO>{});
+    if constexpr (HI - LO <= LEAF) {
+        float r = f(std::integral_constant<int, LO>{});
+        static_for<LO + 1, HI>([&](auto ic) { r = MAX ? fmaxf(r, f(ic)) : fminf(r, f(ic)); });
+        return r;
     } else {
         constexpr int MID = LO + (HI - LO + 1) / 2;
-        const float a = tree_minmax<LO, MID, MAX>(f), b = tree_minmax<MID, HI, MAX>(f);
+        const float a = tree_minmax<LO, MID, MAX, LEAF>(f), b = tree_minmax<MID, HI, MAX, LEAF>(f);
         return MAX ? fmaxf(a, b) : fminf(a, b);
     }
 }
 
-// (7x7 keeps the sequential scan: the tree's wider live set spills there)
 template <int N, bool PAY, bool ZX, typename FV, typename FC, typename FA, typename FL>
 __device__ __forceinline__ Pick pick(FV val, FC col, FA pa, FL pl)
 {
-    constexpr bool TREE = N <= 25;
-    Pick r;
-    if constexpr (TREE) {
-        r = pick_range<0, N, PAY>(val, col, pa, pl);
-    } else {
-        r.v1 = val(std::integral_constant<int, 0>{});
-        r.i1 = 0;
-        r.k1 = col(std::integral_constant<int, 0>{});
-        if constexpr (PAY) {
-            r.xa = pa(std::integral_constant<int, 0>{});
-            r.xl = pl(std::integral_constant<int, 0>{});
-        }
-        static_for<1, N>([&](auto ic) {
-            constexpr int i = decltype(ic)::value;
-            const float v = val(ic);
-            const bool p = v < r.v1;
-            r.v1 = p ? v : r.v1;
-            r.i1 = p ? i : r.i1;
-            r.k1 = p ? col(ic) : r.k1;
-            if constexpr (PAY) {
-                r.xa = p ? pa(ic) : r.xa;
-                r.xl = p ? pl(ic) : r.xl;
-            }
-        });
-    }
+    constexpr int LEAF = N <= 25 ? 1 : N;
+    Pick r = pick_range<0, N, LEAF, PAY>(val, col, pa, pl);
     const uint32_t k1 = r.k1;
-    if constexpr (TREE) {
-        auto masked = [&](auto ic) {
-            return (col(ic) != k1 && (!ZX || val(ic) > 0.f)) ? val(ic) : __int_as_float(0x7f800000);
-        };
-        r.other = tree_minmax<0, N, false>(masked);
-    } else {
-        r.other = __int_as_float(0x7f800000);
-        static_for<0, N>([&](auto ic) {
-            if (col(ic) != k1 && (!ZX || val(ic) > 0.f)) r.other = fminf(r.other, val(ic));
-        });
-    }
+    auto masked = [&](auto ic) {
+        return (col(ic) != k1 && (!ZX || val(ic) > 0.f)) ? val(ic) : __int_as_float(0x7f800000);
+    };
+    r.other = tree_minmax<0, N, false, LEAF>(masked);
     return r;
 }
 
@@ -636,9 +622,7 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
         const float w0 = kp.w[0], w1 = kp.w[1], w2 = kp.w[2];
         // largest Minkowski factor of any product (w0 >= w1 >= w2 >= 0)
         auto lf = [&](auto ic) { return fmaf(w0, LD(ic), L(ic)); };
-        float lmax = 0.f;
-        if constexpr (N <= 25) lmax = fmaxf(tree_minmax<0, N, true>(lf), 0.f);
-        else static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, lf(ic)); });
+        const float lmax = fmaxf(tree_minmax<0, N, true, N <= 25 ? 1 : N>(lf), 0.f);
         const Pick sd = pick<N, false, ZX>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
         const Pick s0 = pick<N, true, ZX>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
                                       col, AD, LD);
@@ -667,9 +651,7 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
         // filters.py:296-328: argmin (A + w AD)(L + w LD), w = n - 2k + 1
         const float w0 = kp.w[0];
         auto lf = [&](auto ic) { return fmaf(w0, LD(ic), L(ic)); };
-        float lmax = 0.f;
-        if constexpr (N <= 25) lmax = fmaxf(tree_minmax<0, N, true>(lf), 0.f);
-        else static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, lf(ic)); });
+        const float lmax = fmaxf(tree_minmax<0, N, true, N <= 25 ? 1 : N>(lf), 0.f);
         const Pick s = pick<N, false, ZX>([&](auto ic) { return fmaf(w0, AD(ic), A(ic)) * fmaf(w0, LD(ic), L(ic)); },
                                       col, none, none);
         kc = s.k1;
@@ -681,9 +663,7 @@ __device__ __forceinline__ void select_window(const KParams &kp, FA A, FL L, FAD
         kc = s.k1;
         doubt = s.doubtful(er, 0.f);
     } else if constexpr (FAM == FAM_DDF) {
-        float lmax = 0.f;
-        if constexpr (N <= 25) lmax = fmaxf(tree_minmax<0, N, true>(L), 0.f);
-        else static_for<0, N>([&](auto ic) { lmax = fmaxf(lmax, L(ic)); });
+        const float lmax = fmaxf(tree_minmax<0, N, true, N <= 25 ? 1 : N>(L), 0.f);
         const Pick s = pick<N, false, ZX>([&](auto ic) { return A(ic) * L(ic); }, col, none, none);
         kc = s.k1;
         doubt = s.doubtful(2.f * er, 2.f * ea * lmax);
