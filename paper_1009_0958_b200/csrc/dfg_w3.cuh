@@ -295,11 +295,18 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
         if ((unsigned)gy >= (unsigned)kp.global_H) gy = resolve_idx(gy, kp.global_H, kp.border);
         return min(max(gy - kp.in_row0, 0), kp.in_rows - 1);
     };
+    // chunks whose rows oy0 - 1 .. oy1 need no border resolution (all but the
+    // first and last chunk of a strip) advance the pixel pointer by one row
+    // per step
+    const int gy_lo = kp.out_row0 + oy0 - 1, gy_hi = kp.out_row0 + oy1;
+    const bool interior = gy_lo >= 0 && gy_lo >= kp.in_row0 && gy_hi < kp.global_H && gy_hi < kp.in_row0 + kp.in_rows;
+    const uint8_t *npx = cbase;
     auto load_px = [&](int yy, uint32_t &r, uint32_t &g, uint32_t &b) {
-        const uint8_t *px = cbase + (size_t)((unsigned long long)(unsigned)row_of(yy) * pitch);
-        r = px[0];
-        g = px[1];
-        b = px[2];
+        if (interior && yy != oy0 - 1) npx += pitch;
+        else npx = cbase + (size_t)((unsigned long long)(unsigned)row_of(yy) * pitch);
+        r = npx[0];
+        g = npx[1];
+        b = npx[2];
     };
     // HIO: in-range columns [c_lo, c_hi) of this strip arrive as the aligned
     // words covering their bytes (an aligned word never crosses a page, so
@@ -394,8 +401,13 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
         pv.y = pk2(__shfl_down_sync(0xffffffffu, pm1.y, 2), __shfl_down_sync(0xffffffffu, pm2.y, 2));
         pv.z = pk2(__shfl_down_sync(0xffffffffu, pm1.z, 2), __shfl_down_sync(0xffffffffu, pm2.z, 2));
         pv.aux = pk2(__shfl_down_sync(0xffffffffu, pm1.aux, 2), __shfl_down_sync(0xffffffffu, pm2.aux, 2));
-        auto eval = [&](auto zc_c) {
+        // LV: 2 = every pair; 1 = the chunk's second warm-up row (the window
+        // of its first output reaches one row up: du <= 1 and the vertical
+        // pair's upper half); 0 = its first warm-up row (du = 0 only)
+        auto eval = [&](auto zc_c, auto lv_c) {
             constexpr bool ZC = decltype(zc_c)::value;
+            constexpr int LV = decltype(lv_c)::value;
+            auto need = [](int t) { return LV == 2 || t == 0 || (LV == 1 && t != 3 && t != 4); };
             auto put = [&](int k, float a, float l) {
                 DT v;
                 if constexpr (BOTH) v = make_float2(a, l);
@@ -411,6 +423,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
             Pair2 pp[6];
 #pragma unroll
             for (int t = 0; t < 5; t++) {
+                if (!need(t)) continue;
                 const ulonglong2 A2 = lds_u2(rA + rsl[t] * C::LANES_E + els[t] + lane);
                 const ulonglong2 B2 = lds_u2(rB + rsl[t] * C::LANES_E + els[t] + lane);
                 pp[t] = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
@@ -418,23 +431,35 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
             pp[5] = pv;
             P2 da[6], dl[6];
 #pragma unroll
-            for (int t = 0; t < 6; t++) pair_values2<FAM, ST, PC, ZC>(q, pp[t], kp, da[t], dl[t]);
+            for (int t = 0; t < 6; t++)
+                if (need(t)) pair_values2<FAM, ST, PC, ZC>(q, pp[t], kp, da[t], dl[t]);
             // du = 0: partners (l-2, l-1) = dv 2, 1
             put(w3_k(0, 2), lo2(da[0]), lo2(dl[0]));
             put(w3_k(0, 1), hi2(da[0]), hi2(dl[0]));
 #pragma unroll
             for (int du = 1; du <= 2; du++) {
                 const int t = 1 + 2 * (du - 1);
+                if (!need(t)) continue;
                 put(w3_k(du, 2), lo2(da[t]), lo2(dl[t]));  // partners l-2, l-1 -> dv = 2, 1
                 put(w3_k(du, 1), hi2(da[t]), hi2(dl[t]));
                 put(w3_k(du, 0), lo2(da[t + 1]), lo2(dl[t + 1]));  // partners l, l+1 -> dv = 0, -1
                 put(w3_k(du, -1), hi2(da[t + 1]), hi2(dl[t + 1]));
             }
-            put(w3_k(1, -2), lo2(da[5]), lo2(dl[5]));  // vertical pair: partner l+2 in rows y-1, y-2
-            put(w3_k(2, -2), hi2(da[5]), hi2(dl[5]));
+            if (need(5)) {
+                put(w3_k(1, -2), lo2(da[5]), lo2(dl[5]));  // vertical pair: partner l+2 in rows y-1, y-2
+                if (LV == 2) put(w3_k(2, -2), hi2(da[5]), hi2(dl[5]));
+            }
         };
-        if (zchk) eval(std::true_type{});
-        else eval(std::false_type{});
+        // warm-up rows take the zero-checking path (correct with or without
+        // zero pixels) so only the full-row variant is instantiated twice
+        if (y > oy0) {
+            if (zchk) eval(std::true_type{}, std::integral_constant<int, 2>{});
+            else eval(std::false_type{}, std::integral_constant<int, 2>{});
+        } else if (y == oy0) {
+            eval(std::integral_constant<bool, C::NEED_L>{}, std::integral_constant<int, 1>{});
+        } else {
+            eval(std::integral_constant<bool, C::NEED_L>{}, std::integral_constant<int, 0>{});
+        }
         pm2 = pm1;
         pm1 = q;
         __syncwarp();
