@@ -12,8 +12,9 @@ call raises ``RuntimeError``.
 Device-resident entry points for pipelines (inputs already in HBM):
 ``filter_device`` (one (H, W, 3) uint8 tensor), ``filter_batch_device``
 ((B, H, W, 3)), ``filter_rows_device`` (a row strip of a taller image, used by
-the multi-GPU strip sharding in ``parallel.py``), and ``filter_host`` (the C
-ABI's host-buffer path: H2D + filter + D2H in one call).
+the multi-GPU strip sharding in ``parallel.py``), ``filter_host`` (the C
+ABI's host-buffer path: H2D + filter + D2H in one call) and
+``filter_host_frames`` (a stream of host frames with up to three in flight).
 """
 
 from __future__ import annotations
@@ -230,7 +231,6 @@ def filter_host_frames(frames, spec, policy=REPLICATE, out=None, stream=None):
     flight, so frame f's copy to the device overlaps frame f-1's kernel and
     frame f-2's copy back; pin the buffers for the overlap.  Each output
     equals ``filter_host`` of its frame."""
-    torch = _torch()
     prm = _params(spec, policy)
     ins = [f for f in frames]
     if not ins:
@@ -248,6 +248,7 @@ def filter_host_frames(frames, spec, policy=REPLICATE, out=None, stream=None):
         if len(out) != len(ins) or any(type(o) is not np.ndarray or o.dtype != np.uint8 or o.shape != shape or
                                        not o.flags.c_contiguous or not o.flags.writeable for o in out):
             raise ValueError("out must hold one writable C-contiguous uint8 array per frame, of the frames' shape")
+    torch = _torch()  # arguments are checked first (ValueError with or without a device)
     n = len(ins)
     pin = (ctypes.c_void_p * n)(*[a.ctypes.data for a in ins])
     pout = (ctypes.c_void_p * n)(*[o.ctypes.data for o in out])

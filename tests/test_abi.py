@@ -117,3 +117,35 @@ def test_cr_acos_is_correctly_rounded():
         glibc_off += math.acos(z) != cr
     # glibc's acos (the reference's) is correctly rounded on all but ~0.1-0.2 %
     assert glibc_off < 0.005 * len(zs)
+
+
+def test_frame_stream_validates_before_any_cuda_call():
+    """dfg_filter_host_frames rejects bad arguments (DFG_E_ARG) before it
+    allocates or touches the device; an empty stream is a no-op."""
+    L = _lib.lib()
+    prm = _lib.params_from_spec(parse_filter_spec("ddf:exact"), "replicate")
+    buf = (ctypes.c_uint8 * 48)()
+    ptrs = (ctypes.c_void_p * 2)(ctypes.addressof(buf), None)
+    assert L.dfg_filter_host_frames(ptrs, ptrs, 0, 4, 4, ctypes.byref(prm), None) == 0
+    assert L.dfg_filter_host_frames(ptrs, ptrs, -1, 4, 4, ctypes.byref(prm), None) == -1
+    assert L.dfg_filter_host_frames(ptrs, ptrs, 1, 0, 4, ctypes.byref(prm), None) == -1
+    assert L.dfg_filter_host_frames(None, ptrs, 1, 4, 4, ctypes.byref(prm), None) == -1
+    assert L.dfg_filter_host_frames(ptrs, ptrs, 2, 4, 4, ctypes.byref(prm), None) == -1  # null frame pointer
+    assert b"frame" in L.dfg_last_error()
+    bad = _lib.params_from_spec(parse_filter_spec("ddf:exact"), "replicate")
+    bad.window = 4
+    assert L.dfg_filter_host_frames(ptrs, ptrs, 1, 4, 4, ctypes.byref(bad), None) == -1
+
+
+def test_frame_stream_python_validation():
+    from paper_1009_0958_b200 import filter_host_frames
+    s = parse_filter_spec("bvdf:exact")
+    a = np.zeros((4, 5, 3), np.uint8)
+    with pytest.raises(ValueError):
+        filter_host_frames([a, np.zeros((4, 6, 3), np.uint8)], s)  # shapes differ
+    with pytest.raises(ValueError):
+        filter_host_frames([a.astype(np.float64)], s)
+    with pytest.raises(ValueError):
+        filter_host_frames([a], s, out=[a, a])  # one output per frame
+    with pytest.raises(ValueError):
+        filter_host_frames([np.zeros((4, 5), np.uint8)], s)
