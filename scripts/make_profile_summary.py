@@ -10,10 +10,10 @@ from pathlib import Path
 tag, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
 out = [f"# ncu summaries, round {tag}", "",
        "Captured on one B200 (sm_100a, driver 580.159) through `gpurun` with "
-       "`ncu --set full --clock-control none --import-source on -k regex:dfg_ -s 3 -c 1` on "
+       "`ncu --set full --clock-control none --import-source on -k "regex:dfg_w3_kernel|dfg_fast_kernel" -s 3 -c 1` on "
        "`python bench.py --config <c> --steps 1 --warmup 3 --no-cpu` (the 4th launch: after the 3 warm-up steps), "
        "and the launch list with `--metrics gpu__time_duration.sum,... --clock-control none -c 400` on the default "
-       "bench command (`scripts/gpu_profiles.sh`). "
+       "bench command (`scripts/gpu_final.sh`). "
        "Durations under ncu are cold-cache and serialised; the bench numbers come from CUDA events without ncu.", ""]
 
 # launch list shares
@@ -35,7 +35,7 @@ for k, m in sorted(agg.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.su
                f"{m.get('launch__registers_per_thread', ['-'])[0]} | {dr / 1e6:.2f} MB |")
 out.append("")
 out.append("(`at::vectorized_elementwise_kernel` is bench.py's 256 MiB L2 flush between timed steps, "
-           "outside the timed events.)")
+           "outside the timed events; `spin_kernel` is the device-side sleep that precedes each start event so the host launch path stays off the measured interval.)")
 out.append("")
 
 KEYS = [("gpu__time_duration.sum", "duration"), ("smsp__inst_executed.sum", "warp instructions"),
