@@ -259,3 +259,32 @@ def test_host_frame_stream(cuda, spec):
         for a, g in zip(imgs, got):
             assert (g == oracle.filter_image(a, s)).all(), (spec, n, pinned)
     assert filter_host_frames([], s) == []
+
+
+@pytest.mark.parametrize("config", ["c1", "c2", "c3", "c4_bvdf_minimax", "c4_bvdf_rgb", "c4_ddf_minimax",
+                                    "c4_ddf_rgb", "c5a", "c5b"])
+def test_config_size_sampled_rows_against_oracle(cuda, config):
+    """Parity at the BASELINE full sizes: the whole config frame (C5b: 3 of
+    its frames) is filtered on the GPU exactly as bench.py does; the oracle
+    re-filters sampled full-width row bands -- both image edges and two
+    interior bands at seeded positions -- from the same frame, and every
+    pixel must match bit for bit."""
+    torch = cuda
+    cfg = synth.CONFIGS[config]
+    s = parse_filter_spec(cfg["spec"])
+    h = s.window // 2
+    x = synth.config_input(config, frames=3 if config == "c5b" else None)
+    if x.ndim == 4:
+        got = filter_batch_device(torch.from_numpy(x).cuda(), s).cpu().numpy()
+        frames = list(zip(x, got))
+    else:
+        frames = [(x, filter_device(torch.from_numpy(x).cuda(), s).cpu().numpy())]
+    rng = np.random.default_rng(sum(map(ord, config)))
+    for img, out in frames:
+        H = img.shape[0]
+        bands = [(0, 4), (H - 4, H)] + [(r, r + 6) for r in rng.integers(8, H - 16, size=2)]
+        for r0, r1 in bands:
+            b0, b1 = max(0, r0 - h), min(H, r1 + h)
+            want = oracle.filter_image(img[b0:b1], s, rows=(r0 - b0, r1 - b0))[r0 - b0:r1 - b0]
+            bad = int((out[r0:r1] != want).any(-1).sum())
+            assert bad == 0, (config, r0, r1, bad)
