@@ -288,3 +288,31 @@ def test_config_size_sampled_rows_against_oracle(cuda, config):
             want = oracle.filter_image(img[b0:b1], s, rows=(r0 - b0, r1 - b0))[r0 - b0:r1 - b0]
             bad = int((out[r0:r1] != want).any(-1).sum())
             assert bad == 0, (config, r0, r1, bad)
+
+
+def test_w3_deferred_queue_mode_subprocess(cuda, tmp_path):
+    """The opt-in deferred re-decision queue of the 3x3 row sweep
+    (DFG_W3_QUEUE=1, read once per process) reproduces the oracle, and a
+    second call on the same workspace starts from a clean queue."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parent.parent
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import numpy as np, torch, oracle\n"
+        "from paper_1009_0958_b200 import filter_device, last_fixup_count, parse_filter_spec, synth\n"
+        "for spec in ('ddf:exact', 'acwddf:exact', 'bvdf:minimax'):\n"
+        "    s = parse_filter_spec(spec)\n"
+        "    img = synth.noisy_image(600, 300, 9, ('uncorrelated', 0.15))\n"
+        "    want = oracle.filter_image(img, s)\n"
+        "    x = torch.from_numpy(img).cuda()\n"
+        "    last_fixup_count()\n"
+        "    for _ in range(2):\n"
+        "        got = filter_device(x, s).cpu().numpy()\n"
+        "        assert (got == want).all(), spec\n"
+        "    assert last_fixup_count() > 0, spec\n"
+        "print('ok')\n" % str(root))
+    env = dict(__import__("os").environ, DFG_W3_QUEUE="1", DFG_S3_KERNEL="w3")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
