@@ -316,3 +316,19 @@ def test_w3_deferred_queue_mode_subprocess(cuda, tmp_path):
     env = dict(__import__("os").environ, DFG_W3_QUEUE="1", DFG_S3_KERNEL="w3")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("spec", ["ddf:exact", "acwddf:minimax:window=5", "bvdf:rgb:window=7"])
+@pytest.mark.parametrize("shape", [(6, 24001), (9000, 5), (2, 3), (1, 4097), (4097, 1)])
+def test_extreme_aspect_ratios(cuda, spec, shape):
+    """Very wide / very tall / tiny frames (grids with a single strip or a
+    single tile row, windows larger than the image, both borders) through
+    the device and host paths."""
+    torch = cuda
+    s = parse_filter_spec(spec)
+    img = synth.noisy_image(*shape, 41, ("correlated", 0.2))
+    for border in ("replicate", "reflect"):
+        want = oracle.filter_image(img, s, border)
+        got = filter_device(torch.from_numpy(img).cuda(), s, _policy(border)).cpu().numpy()
+        assert (got == want).all(), (spec, shape, border, int((got != want).any(-1).sum()))
+        assert (filter_host(img, s, _policy(border)) == want).all(), (spec, shape, border)
