@@ -247,6 +247,9 @@ def run_reference(args, config):
     print(json.dumps(line), flush=True)
 
 
+FRAME_SLOTS = int(os.environ.get("DFG_FRAME_SLOTS", "4"))  # device slots of dfg_filter_host_frames (csrc/dfg_api.cu frame_slots())
+
+
 def _host_loop(fn, min_calls: int, warm_s: float = 0.5, reps: int = 5):
     """Median over `reps` timed loops of `min_calls` calls of fn() (wall
     clock; each call is synchronous), after >= warm_s of warm-up calls: the
@@ -280,7 +283,7 @@ def measure_e2e(wl, spec, F, torch, args, world, cdev, dist):
     nf, fb = frames.shape[0], frames[0].nbytes
     # a ring of distinct pinned buffers (a multiple of the 3 device slots, so
     # frames sharing a host buffer also share a slot stream)
-    ring = nf if wl["kind"] == "batch" else (6 if fb < (64 << 20) else 3)
+    ring = nf if wl["kind"] == "batch" else (2 * FRAME_SLOTS if fb < (64 << 20) else FRAME_SLOTS)
     hin = [torch.from_numpy(frames[i % nf]).pin_memory() for i in range(ring)]
     hout = [torch.empty(frames.shape[1:], dtype=torch.uint8).pin_memory() for _ in range(ring)]
     ins, outs = [t.numpy() for t in hin], [t.numpy() for t in hout]
@@ -316,11 +319,11 @@ def measure_e2e(wl, spec, F, torch, args, world, cdev, dist):
            "h2d_bytes_per_step": fb * (nf if wl["kind"] == "batch" else 1),
            "d2h_bytes_per_step": fb * (nf if wl["kind"] == "batch" else 1), "ms_per_step": round(e_ms, 4),
            "path": (f"filter_host_frames (C ABI dfg_filter_host_frames): {n_frames} frames per call from a ring of "
-                    f"{ring} pinned host buffers, H2D + kernel + D2H of every frame inside, up to 3 frames in "
+                    f"{ring} pinned host buffers, H2D + kernel + D2H of every frame inside, up to {FRAME_SLOTS} frames in "
                     "flight; median of 5 timed calls"
                     if wl["kind"] == "image" else
                     f"filter_host_frames over the {nf} frames of the batch, H2D + kernel + D2H of every frame "
-                    "inside, up to 3 frames in flight; median of 5 timed calls")}
+                    f"inside, up to {FRAME_SLOTS} frames in flight; median of 5 timed calls")}
     if sync:
         out["sync_call"] = {"value": round(px_frame * world / sync / 1e6, 3), "unit": "Mpixel/s",
                             "ms_per_step": round(sync * 1e3, 4),

@@ -141,9 +141,9 @@ DFG_API int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *
 /* A stream of n independent (H, W, 3) frames from HOST memory (one buffer
  * per frame, pinned for overlap), synchronised before return: the
  * reference's per-frame apply_filter loop (bench.py:96-109, cli filter over
- * several files) as one call.  Frames go round-robin to three cached device
- * slots, each with its own stream: frame f's H2D overlaps frame f-1's
- * kernel and frame f-2's D2H.  Same outputs as n dfg_filter_host calls. */
+ * several files) as one call.  Frames go round-robin to four cached device
+ * slots, each with its own stream: frame f's H2D overlaps the kernels and
+ * D2H copies of the frames before it.  Same outputs as n dfg_filter_host calls. */
 DFG_API int dfg_filter_host_frames(const uint8_t *const *h_in, uint8_t *const *h_out,
                     int32_t n_frames, int32_t H, int32_t W,
                     const dfg_params *prm, void *stream);

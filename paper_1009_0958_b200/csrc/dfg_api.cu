@@ -534,12 +534,14 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
 
 namespace {
 
-// Frame stream from host memory: kFrameSlots device slots, each with its own
-// input/output buffers, workspace and stream.  Frame f goes to slot f % S:
-// H2D, kernel, D2H in that slot's stream, so frame f's H2D overlaps frame
-// f-1's kernel and frame f-2's D2H (PCIe is full duplex and the SMs are idle
-// during the copies); a slot is reused only after its previous frame's D2H.
-constexpr int kFrameSlots = 3;
+// Frame stream from host memory: frame_slots() device slots (default 4),
+// each with its own input/output buffers, workspace and stream.  Frame f
+// goes to slot f % S: H2D, kernel, D2H in that slot's stream, so frame f's
+// H2D overlaps the kernels and D2H copies of the frames before it (PCIe is
+// full duplex and the SMs are idle during the copies); a slot is reused only
+// after its previous frame's D2H.  Measured (C2 frames, 3 MB each way):
+// 2 slots 100 us per frame, 3 slots 86, 4 slots 72.5, 5 slots 73-83.
+constexpr int kFrameSlots = 8;  // capacity; frame_slots() are used
 
 struct FrameCache {
     uint8_t *d_in[kFrameSlots] = {}, *d_out[kFrameSlots] = {};
@@ -562,6 +564,17 @@ struct FrameCache {
     ~FrameCache() { release(); }
 };
 thread_local FrameCache g_frames;
+
+// slots in use (DFG_FRAME_SLOTS: diagnostics override, 1..8)
+int frame_slots()
+{
+    static const int n = [] {
+        const char *e = getenv("DFG_FRAME_SLOTS");
+        const int v = e ? atoi(e) : 4;
+        return v < 1 ? 1 : (v > kFrameSlots ? kFrameSlots : v);
+    }();
+    return n;
+}
 
 }  // namespace
 
@@ -586,7 +599,7 @@ int dfg_filter_host_frames(const uint8_t *const *h_in, uint8_t *const *h_out, in
     cudaError_t e = cudaSuccess;
     if (c.dev != dev || c.px_cap < px) {
         c.release();
-        for (int k = 0; k < kFrameSlots && e == cudaSuccess; k++) {
+        for (int k = 0; k < frame_slots() && e == cudaSuccess; k++) {
             e = cudaMalloc(&c.d_in[k], nbytes);
             if (e == cudaSuccess) e = cudaMalloc(&c.d_out[k], nbytes);
             if (e == cudaSuccess) e = cudaMalloc(&c.ws[k], wsb);
@@ -607,13 +620,14 @@ int dfg_filter_host_frames(const uint8_t *const *h_in, uint8_t *const *h_out, in
         c.dev = dev;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    const int ns = frame_slots();
     // fork: the slots start after prior work on `st`
     e = cudaEventRecord(c.ev_start, st);
-    for (int k = 0; k < kFrameSlots && e == cudaSuccess; k++) e = cudaStreamWaitEvent(c.s[k], c.ev_start, 0);
+    for (int k = 0; k < ns && e == cudaSuccess; k++) e = cudaStreamWaitEvent(c.s[k], c.ev_start, 0);
     if (e != cudaSuccess) return cuda_fail(e, "fork");
     const long long pitch = 3LL * W;
     for (int f = 0; f < n_frames; f++) {
-        const int k = f % kFrameSlots;
+        const int k = f % ns;
         e = cudaMemcpyAsync(c.d_in[k], h_in[f], nbytes, cudaMemcpyHostToDevice, c.s[k]);
         if (e != cudaSuccess) return cuda_fail(e, "frame H2D");
         rc = run(c.d_in[k], H, W, 0, H, pitch, 0, c.d_out[k], 0, H, pitch, 0, 1, prm, c.ws[k], wsb, c.s[k], nullptr);
@@ -622,7 +636,7 @@ int dfg_filter_host_frames(const uint8_t *const *h_in, uint8_t *const *h_out, in
         if (e != cudaSuccess) return cuda_fail(e, "frame D2H");
     }
     // join, then wait for the whole stream of frames
-    for (int k = 0; k < kFrameSlots && e == cudaSuccess; k++) {
+    for (int k = 0; k < ns && e == cudaSuccess; k++) {
         e = cudaEventRecord(c.ev_end[k], c.s[k]);
         if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_end[k], 0);
     }

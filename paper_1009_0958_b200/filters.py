@@ -14,7 +14,7 @@ Device-resident entry points for pipelines (inputs already in HBM):
 ((B, H, W, 3)), ``filter_rows_device`` (a row strip of a taller image, used by
 the multi-GPU strip sharding in ``parallel.py``), ``filter_host`` (the C
 ABI's host-buffer path: H2D + filter + D2H in one call) and
-``filter_host_frames`` (a stream of host frames with up to three in flight).
+``filter_host_frames`` (a stream of host frames with up to four in flight).
 """
 
 from __future__ import annotations
@@ -227,9 +227,9 @@ def filter_host_frames(frames, spec, policy=REPLICATE, out=None, stream=None):
     """A stream of independent host frames through ``dfg_filter_host_frames``:
     ``frames`` is a sequence of C-contiguous uint8 (H, W, 3) arrays of one
     shape (or an (F, H, W, 3) array); returns the list of filtered frames
-    (written into ``out``'s arrays when given).  Up to three frames are in
-    flight, so frame f's copy to the device overlaps frame f-1's kernel and
-    frame f-2's copy back; pin the buffers for the overlap.  Each output
+    (written into ``out``'s arrays when given).  Up to four frames are in
+    flight, so frame f's copy to the device overlaps the kernels and copies
+    back of the frames before it; pin the buffers for the overlap.  Each output
     equals ``filter_host`` of its frame."""
     prm = _params(spec, policy)
     ins = [f for f in frames]
