@@ -675,10 +675,18 @@ cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KP
         const char *e = getenv("DFG_W3_RPC");  // diagnostics only
         return e ? atoi(e) : 0;
     }();
-    const long long wps = env_wps > 0 ? env_wps : 2 * minb;
-    const long long slots = 148 * wps;
     const long long cols = (long long)n_strips * kp.n_frames;  // independent strip columns
     const long long strip_rows = cols * kp.out_rows;
+    // small single-wave frames (< 8 rows per chunk at 16 warps per SM): 12
+    // warps per SM with longer chunks (C1 512^2: 22.6 -> 21.0 us; C2's 15-row
+    // chunks stay at 16 warps: 12 measured 4.5 % slower there)
+    static const int small_wps = [] {
+        const char *e = getenv("DFG_W3_SMALL_WPS");  // diagnostics only
+        return e ? atoi(e) : 12;
+    }();
+    long long wps = env_wps > 0 ? env_wps : 2 * minb;
+    if (env_wps <= 0 && small_wps > 0 && strip_rows < 8LL * 148 * wps) wps = small_wps;
+    const long long slots = 148 * wps;
     const long long waves = (strip_rows + slots * 64 - 1) / (slots * 64);
     long long n_chunks = (waves * slots) / cols;
     const int rpc_hint = rpc_env > 0 ? rpc_env : kp.w3_rpc;  // host pipeline bands: short chunks
