@@ -10,7 +10,7 @@ from pathlib import Path
 tag, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
 out = [f"# ncu summaries, round {tag}", "",
        "Captured on one B200 (sm_100a, driver 580.159) through `gpurun` with "
-       "`ncu --set full --clock-control none --import-source on -k "regex:dfg_w3_kernel|dfg_fast_kernel" -s 3 -c 1` on "
+       "`ncu --set full --clock-control none --import-source on -k 'regex:dfg_w3_kernel|dfg_fast_kernel' -s 3 -c 1` on "
        "`python bench.py --config <c> --steps 1 --warmup 3 --no-cpu` (the 4th launch: after the 3 warm-up steps), "
        "and the launch list with `--metrics gpu__time_duration.sum,... --clock-control none -c 400` on the default "
        "bench command (`scripts/gpu_final.sh`). "
