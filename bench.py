@@ -163,21 +163,45 @@ def workload(config: str, rank: int, world: int):
     return {"kind": "image", "x": img, "px": H * W, "total_px": H * W * world, "scaling": "weak"}
 
 
-def cpu_rate(img: np.ndarray, spec, budget_s: float, threads: int, min_rows: int = 4):
-    """Time the float64 oracle (the reference algorithm restated in C) on
-    full-width row bands of ``img`` for about ``budget_s`` seconds."""
+def oracle_band(img: np.ndarray, spec, r0: int, rows: int, threads: int) -> float:
+    """Seconds for the oracle to filter output rows [r0, r0 + rows) of ``img``
+    from the band holding them and their halo rows (the float64 conversion
+    scales with the band, not the frame)."""
     import oracle
 
-    H, W = img.shape[:2]
+    H = img.shape[0]
+    h = spec.window // 2 if getattr(spec, "family", "identity") != "identity" else 0
+    b0, b1 = max(0, r0 - h), min(H, r0 + rows + h)
+    t = time.perf_counter()
+    oracle.filter_image(img[b0:b1], spec, threads=threads, rows=(r0 - b0, r0 - b0 + rows))
+    return time.perf_counter() - t
+
+
+def cpu_rows_for(img: np.ndarray, spec, seconds: float, threads: int, min_rows: int = 4) -> int:
+    """Full-width rows the oracle filters in about ``seconds``."""
+    H = img.shape[0]
     rows = min(H, min_rows)
-    t0 = time.perf_counter()
-    oracle.filter_image(img, spec, threads=threads, rows=(0, rows))
-    dt = time.perf_counter() - t0
-    rows2 = int(min(H, max(rows, rows * budget_s / max(dt, 1e-6))))
-    t0 = time.perf_counter()
-    oracle.filter_image(img, spec, threads=threads, rows=(0, rows2))
-    dt = time.perf_counter() - t0
-    return rows2 * W / dt / 1e6, rows2, dt
+    dt = oracle_band(img, spec, 0, rows, threads)
+    return int(min(H, max(rows, rows * seconds / max(dt, 1e-6))))
+
+
+def cpu_rate(img: np.ndarray, spec, budget_s: float, threads: int, min_rows: int = 4):
+    """Time the float64 oracle (the reference algorithm restated in C) on a
+    full-width row band of ``img`` (the top band plus its halo rows, so the
+    conversion to float64 scales with the band, not the frame), repeating
+    the band until about ``budget_s`` seconds of CPU work have run.
+    Returns (Mpixel/s, rows per pass, passes, seconds)."""
+    W = img.shape[1]
+
+    def run(rows):
+        return oracle_band(img, spec, 0, rows, threads)
+
+    rows = cpu_rows_for(img, spec, 0.25 * budget_s, threads, min_rows)  # one pass <= ~1/4 of the budget
+    passes, total = 0, 0.0
+    while passes < 2 or total < budget_s:
+        total += run(rows)
+        passes += 1
+    return rows * W * passes / total / 1e6, rows, passes, total
 
 
 def c4_quality(config, spec, x, out, F, torch):
@@ -219,15 +243,11 @@ def run_reference(args, config):
     threads = os.cpu_count() or 1
     # size each step so the whole --steps/--warmup run stays within ~2 minutes
     per_step_s = max(0.5, min(10.0, 120.0 / (args.steps + args.warmup)))
-    _, rows, _ = cpu_rate(img, spec, per_step_s, threads)
+    rows = cpu_rows_for(img, spec, per_step_s, threads)
     times = []
     for k in range(args.warmup + args.steps):
         r0 = (k * rows) % max(1, H - rows + 1)
-        t0 = time.perf_counter()
-        import oracle
-
-        oracle.filter_image(img, spec, threads=threads, rows=(r0, r0 + rows))
-        dt = time.perf_counter() - t0
+        dt = oracle_band(img, spec, r0, rows, threads)
         if k >= args.warmup:
             times.append(dt)
     px = rows * W
@@ -464,10 +484,11 @@ def run_ours(args, config):
     if world == 1 and not args.no_cpu:
         img = wl["x"][0] if wl["x"].ndim == 4 else wl["x"]
         threads = os.cpu_count() or 1
-        rate, rows, dt = cpu_rate(img, spec, args.cpu_seconds, threads)
+        rate, rows, passes, dt = cpu_rate(img, spec, args.cpu_seconds, threads)
         cpu = {"value": round(rate, 4), "unit": "Mpixel/s", "cores": threads, "kind": "port",
-               "sample": f"{rows} full-width rows ({rows * img.shape[1]} px) of the {config} frame, {dt:.1f} s, "
-                         "oracle/oracle.c (reference engine restated in C, float64, glibc acos)"}
+               "sample": f"{passes} passes over {rows} full-width rows ({rows * img.shape[1]} px) of the {config} "
+                         f"frame, {dt:.1f} s of CPU work, oracle/oracle.c (reference engine restated in C, "
+                         "float64, glibc acos)"}
     launches = args.steps  # one decision kernel per step (float64 re-decision runs inside it)
     line = {
         "metric": "Mpixel/s per filter/window", "value": round(value, 3), "unit": "Mpixel/s",
