@@ -337,7 +337,11 @@ __device__ __forceinline__ P2 angle_half2(const Pix &p, const Pair2 &q)
     }
     const P2 den = fma2(bc2(pa), qa, dot);  // |a||b| + a.b, one rounding
     const P2 P = mul2(cc, mul2(den, den));
-    const P2 R = pk2(rsqrt_approx(fmaxf(lo2(P), 1e-30f)), rsqrt_approx(fmaxf(hi2(P), 1e-30f)));
+    // P is 0 (parallel: cc = 0) or >= 1 (cc and den^2 are >= 1 for nonzero
+    // integer vectors), so P + 1e-30 is P exactly or 1e-30: max(P, 1e-30)
+    // in one packed add
+    const P2 Pt = add2(P, bc2(1e-30f));
+    const P2 R = pk2(rsqrt_approx(lo2(Pt)), rsqrt_approx(hi2(Pt)));
     return atan01x2_2(mul2(cc, R));  // cc = 0 (parallel) -> exactly 0
 }
 
@@ -351,7 +355,8 @@ __device__ __forceinline__ P2 angle_minimax2(const Pix &p, const Pair2 &q, const
     const float z0 = fminf(lo2(zr), 1.f), z1 = fminf(hi2(zr), 1.f);  // dot >= 0: only the upper clamp bites
     const P2 z = pk2(z0, z1);
     const P2 u = mul2(cc, add2(z, bc2(1.f)));
-    const P2 R = pk2(rsqrt_approx(fmaxf(lo2(u), 1e-30f)), rsqrt_approx(fmaxf(hi2(u), 1e-30f)));
+    const P2 ut = add2(u, bc2(1e-30f));  // u = 0 or u >= cc >= 1: max(u, 1e-30) exactly (angle_half2)
+    const P2 R = pk2(rsqrt_approx(lo2(ut)), rsqrt_approx(hi2(ut)));
     const P2 t = mul2(mul2(cc, R), rnab);
     P2 pa = fma2(bc2(kp.ca[4]), z, bc2(kp.ca[3]));
     pa = fma2(pa, z, bc2(kp.ca[2]));
