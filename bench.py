@@ -1,31 +1,46 @@
 #!/usr/bin/env python
 """Throughput benchmark of the B200 directional-filter path (one JSON line).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5a] [--impl ours|reference]
 
-A "step" is one filter pass over one frame (or the frame batch for c5b) of a
-BASELINE config's seeded synthetic input, resident in HBM.  The default
-workload is BASELINE.json configs[1] (C2: DDF 3x3 exact on a 1024x1024
-image, 15% uncorrelated impulsive noise); ``--config`` selects the others
-(c1, c3, c4_*, c5a, c5b; see paper_1009_0958_b200/synth.py).
+A "step" is one filter pass over one frame (or the 64-frame batch for c5b)
+of a BASELINE config's seeded synthetic input, resident in HBM.  The default
+workload is C5a -- DDF 7x7 exact on an 8192x8192 frame, 20% correlated
+impulsive noise -- the largest single-GPU config and the one BASELINE.json
+quotes its multi-GPU scaling on; ``--config`` selects the others (c1, c2,
+c3, c4_*, c5b; paper_1009_0958_b200/synth.py).
 
 Timing: W untimed warm-up steps, then exactly K steps, each bracketed by CUDA
 events on the launching stream; an L2 flush (a 256 MiB device write) runs
-between timed steps, outside the events, so no step reads its input from a
-warm L2.  The K-step region is bracketed by a barrier and
+between timed steps, outside the events (C5a's 201 MB input is larger than
+the 126 MB L2 anyway).  The K-step region is bracketed by a barrier and
 torch.cuda.synchronize() on both sides; the step time is the MAX over ranks.
 nvidia-smi samples SM clocks and throttle reasons during the timed region.
 
-Multi-GPU (torchrun, one process per GPU): c1-c4 run one replica per rank
-(weak scaling: every rank filters its own frame); c5a shards the 8192-row
-frame into contiguous row strips, each rank holding its strip plus a 3-row
-halo (strong scaling, no collective on the data path); c5b splits the 64
-frames across ranks (strong).
+Multi-GPU: ``--gpus N`` (N > 1) without a torchrun environment re-launches
+this script under ``torch.distributed.run`` with N processes (one per GPU,
+NCCL).  C5a is strip-sharded (strong scaling): every rank starts from its
+own rows only, and the timed step is the north star's whole data path --
+NCCL halo exchange with the neighbours, the strip filter in row chunks, and
+the chunk-by-chunk gather of the filtered rows into rank 0
+(parallel.StripJob); the resident-output variant (no gather) is reported
+beside it.  C5b splits the 64 frames (strong, no collective); C1-C4 run one
+replica per rank (weak).
 
-``--impl reference`` times the reference algorithm's CPU implementation on
-the host cores instead: the float64 C restatement in oracle/ (the reference
-itself is Python+numba and cannot travel to the GPU box), all host threads,
-on bounded row bands of the same input.
+At N=1 rank 0 also reports (outside the timed region): ``e2e`` through the
+C ABI host paths (pinned uint8 host buffers, H2D + D2H inside) and through
+the drop-in ``apply_filter`` (float64 RasterImage in and out);
+``cpu_baseline`` -- the reference's own ``apply_filter`` (numba, from
+baseline/_ref) on the box's host cores at ``workers=os.cpu_count()`` and
+``workers=1``, with the oracle port (oracle/oracle.c) beside it; ``parity``
+-- every output pixel against the float64 oracle (the checker), mismatches
+classified as near-ties; and ``configs``, the same per-config figures for
+every other BASELINE config (``--no-table`` skips them).
+
+``--impl reference`` times the reference's CPU implementation on the host
+cores instead (rank 0 only): the reference package itself when baseline/_ref
+holds it, else the oracle port, all host threads, bounded row samples of
+the same input.
 """
 
 from __future__ import annotations
@@ -34,8 +49,11 @@ import argparse
 import json
 import math
 import os
+import platform
+import socket
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 from pathlib import Path
@@ -57,6 +75,7 @@ WORK = {
     "c4_ddf_rgb": (1705, 80), "c5a": (6601, 168), "c5b": (501, 24),
 }
 BYTES_PER_PX = 6  # 3 B uint8 in + 3 B uint8 out (halo re-reads excluded)
+DEFAULT_CONFIG = "c5a"
 
 
 def peaks():
@@ -141,76 +160,318 @@ def dist_env():
     return ws, rank, local
 
 
+def relaunch_under_torchrun(n: int) -> int:
+    """--gpus N > 1 outside torchrun: one process per GPU on this node."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def config_dict(config: str, world: int):
+    """The workload description both arms print (identical dicts)."""
+    cfg = synth.CONFIGS[config]
+    kind = {"strips": "row strips", "batch": "frame split"}.get(workload_kind(config, world), "replica")
+    return {"workload": config, "spec": cfg["spec"], "shape": list(cfg["shape"]), "noise": list(cfg["noise"]),
+            "seed": cfg["seed"], "frames": cfg.get("frames", 1), "border": "replicate",
+            "l2": "flushed between timed steps (256 MiB write); inputs resident in HBM",
+            "parallelism": f"{kind} x{world}"}
+
+
 def workload(config: str, rank: int, world: int):
-    """(input array for this rank, output pixels of this rank, total pixels, description)."""
+    """This rank's share of a config: kind "image" (a whole frame: one
+    replica per rank), "batch" (C5b frames split across ranks) or "strips"
+    (C5a row strips, N > 1)."""
     cfg = synth.CONFIGS[config]
     H, W = cfg["shape"]
     if config == "c5b":
+        from paper_1009_0958_b200.parallel import frame_split
+
         B = cfg["frames"]
-        per = math.ceil(B / world)
-        f0, f1 = rank * per, min(B, (rank + 1) * per)
+        f0, f1 = frame_split(B, world, rank)
         frames = np.stack([synth.noisy_image(H, W, cfg["seed"] + i, cfg["noise"]) for i in range(f0, f1)])
         return {"kind": "batch", "x": frames, "px": frames.shape[0] * H * W, "total_px": B * H * W,
                 "scaling": "strong" if world > 1 else "weak"}
     img = synth.config_input(config)
     if config == "c5a" and world > 1:
-        h = parse_filter_spec(cfg["spec"]).window // 2
-        per = math.ceil(H / world)
-        r0, r1 = rank * per, min(H, (rank + 1) * per)
-        i0, i1 = max(0, r0 - h), min(H, r1 + h)
-        return {"kind": "rows", "x": np.ascontiguousarray(img[i0:i1]), "in_row0": i0, "out_row0": r0,
-                "out_rows": r1 - r0, "H": H, "px": (r1 - r0) * W, "total_px": H * W, "scaling": "strong"}
+        return {"kind": "strips", "x": img, "H": H, "W": W, "total_px": H * W, "scaling": "strong"}
     return {"kind": "image", "x": img, "px": H * W, "total_px": H * W * world, "scaling": "weak"}
 
 
-def oracle_band(img: np.ndarray, spec, r0: int, rows: int, threads: int) -> float:
-    """Seconds for the oracle to filter output rows [r0, r0 + rows) of ``img``
-    from the band holding them and their halo rows (the float64 conversion
-    scales with the band, not the frame)."""
-    import oracle
+# ---------------------------------------------------------------- CPU side --
 
-    H = img.shape[0]
-    h = spec.window // 2 if getattr(spec, "family", "identity") != "identity" else 0
-    b0, b1 = max(0, r0 - h), min(H, r0 + rows + h)
-    t = time.perf_counter()
-    oracle.filter_image(img[b0:b1], spec, threads=threads, rows=(r0 - b0, r0 - b0 + rows))
-    return time.perf_counter() - t
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    info = {"cpu_model": model, "logical_cores": os.cpu_count(), "numpy": np.__version__}
+    try:
+        import numba
+
+        info["numba"] = numba.__version__
+    except Exception:
+        info["numba"] = None
+    return info
 
 
-def cpu_rows_for(img: np.ndarray, spec, seconds: float, threads: int, min_rows: int = 4) -> int:
-    """Full-width rows the oracle filters in about ``seconds``."""
+_REF = None
+
+
+def reference_module():
+    """The reference package itself (pip-installed into baseline/_ref from
+    /root/reference in the build container; it travels with the repo), or
+    None when it is absent or does not import."""
+    global _REF
+    if _REF is None:
+        p = ROOT / "baseline" / "_ref"
+        _REF = False
+        if (p / "dirfilt").is_dir():
+            os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "dfg_bench_numba"))
+            sys.path.insert(0, str(p))
+            try:
+                import dirfilt
+
+                _REF = dirfilt
+            except Exception as e:  # pragma: no cover - depends on the box
+                print(f"reference package unavailable: {e}", file=sys.stderr)
+    return _REF or None
+
+
+def _band_rows(img, spec_h, seconds, run_rows, min_rows=4):
+    """Full-width rows one call of run_rows(rows) takes about ``seconds`` for."""
     H = img.shape[0]
     rows = min(H, min_rows)
-    dt = oracle_band(img, spec, 0, rows, threads)
+    dt = run_rows(rows)
     return int(min(H, max(rows, rows * seconds / max(dt, 1e-6))))
 
 
-def cpu_rate(img: np.ndarray, spec, budget_s: float, threads: int, min_rows: int = 4):
-    """Time the float64 oracle (the reference algorithm restated in C) on a
-    full-width row band of ``img`` (the top band plus its halo rows, so the
-    conversion to float64 scales with the band, not the frame), repeating
-    the band until about ``budget_s`` seconds of CPU work have run.
-    Returns (Mpixel/s, rows per pass, passes, seconds)."""
+def cpu_reference(img, spec_text, budget_s, workers):
+    """The reference ``apply_filter`` (numba, reference filters.py:379-433)
+    on the top full-width row band of ``img`` (the band as its own image;
+    cost is linear in rows).  JIT compile and thread-pool warm-up first,
+    then the median of >= 3 calls.  Returns (Mpixel/s, rows, calls, s)."""
+    ref = reference_module()
+    spec = ref.parse_filter_spec(spec_text)
     W = img.shape[1]
 
     def run(rows):
-        return oracle_band(img, spec, 0, rows, threads)
+        band = ref.RasterImage(img[:rows].astype(np.float64))
+        t = time.perf_counter()
+        ref.apply_filter(band, spec, workers=workers)
+        return time.perf_counter() - t
 
-    rows = cpu_rows_for(img, spec, 0.25 * budget_s, threads, min_rows)  # one pass <= ~1/4 of the budget
-    passes, total = 0, 0.0
-    while passes < 2 or total < budget_s:
-        total += run(rows)
-        passes += 1
-    return rows * W * passes / total / 1e6, rows, passes, total
+    run(min(img.shape[0], 16))  # compile + warm the pool
+    rows = _band_rows(img, 0, budget_s / 3.0, run)
+    ts = [run(rows) for _ in range(3)]
+    t = float(np.median(ts))
+    return rows * W / t / 1e6, rows, len(ts), sum(ts)
+
+
+def cpu_port(img, spec, budget_s, threads):
+    """The oracle port (oracle/oracle.c: the reference engine restated in C,
+    float64, glibc acos) on the top full-width band (+ halo rows)."""
+    import oracle
+
+    H, W = img.shape[:2]
+    h = spec.window // 2
+
+    def run(rows):
+        t = time.perf_counter()
+        oracle.filter_image(img[:min(H, rows + h)], spec, threads=threads, rows=(0, rows))
+        return time.perf_counter() - t
+
+    rows = _band_rows(img, h, budget_s / 3.0, run)
+    ts = [run(rows) for _ in range(3)]
+    t = float(np.median(ts))
+    return rows * W / t / 1e6, rows, len(ts), sum(ts)
+
+
+def cpu_baseline(img, spec_text, budget_s, full=True):
+    """cpu_baseline of the JSON line: the reference itself at all cores
+    (kind "reference"; workers=1 beside it when ``full``), else the oracle
+    port (kind "port"); the port is also reported when the reference ran."""
+    spec = parse_filter_spec(spec_text)
+    cores = os.cpu_count() or 1
+    W = img.shape[1]
+    out = {}
+    if reference_module() is not None:
+        v, rows, n, dt = cpu_reference(img, spec_text, budget_s, cores)
+        out = {"value": round(v, 4), "unit": "Mpixel/s", "cores": cores, "kind": "reference",
+               "sample": f"reference dirfilt.apply_filter (numba, baseline/_ref) workers={cores} on the top {rows} "
+                         f"full-width rows ({rows * W} px) of the frame, median of {n} calls after JIT warm-up"}
+        if full:
+            v1, rows1, n1, _ = cpu_reference(img, spec_text, budget_s / 2, 1)
+            out["workers_1"] = {"value": round(v1, 4), "unit": "Mpixel/s", "cores": 1,
+                                "sample": f"same, workers=1, {rows1} rows"}
+    vp, rowsp, np_, _ = cpu_port(img, spec, budget_s / (2 if out else 1), cores)
+    port = {"value": round(vp, 4), "unit": "Mpixel/s", "cores": cores, "kind": "port",
+            "sample": f"oracle/oracle.c (the reference engine restated in C, float64, glibc acos) on the top {rowsp} "
+                      f"full-width rows, median of {np_} calls"}
+    if not out:
+        out = port
+    else:
+        out["port"] = port
+    if full:
+        out.update(cpu_info())
+    return out
+
+
+def run_reference(args, config):
+    """--impl reference: the reference's CPU implementation on the host cores
+    (rank 0 only; other ranks exit without work)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = synth.CONFIGS[config]
+    img = synth.config_input(config, frames=1)
+    if img.ndim == 4:
+        img = img[0]
+    H, W = img.shape[:2]
+    cores = os.cpu_count() or 1
+    spec = parse_filter_spec(cfg["spec"])
+    per_step_s = max(0.2, min(2.0, 120.0 / (args.steps + args.warmup)))
+    ref = reference_module()
+    if ref is not None:
+        rspec = ref.parse_filter_spec(cfg["spec"])
+
+        def sample(rows):
+            band = ref.RasterImage(img[:rows].astype(np.float64))
+            t = time.perf_counter()
+            ref.apply_filter(band, rspec, workers=cores)
+            return time.perf_counter() - t
+        sample(min(H, 16))  # JIT compile + pool warm-up
+        kind = "reference"
+        what = f"reference dirfilt.apply_filter (numba, baseline/_ref), workers={cores}"
+    else:
+        import oracle
+
+        h = spec.window // 2
+
+        def sample(rows):
+            t = time.perf_counter()
+            oracle.filter_image(img[:min(H, rows + h)], spec, threads=cores, rows=(0, rows))
+            return time.perf_counter() - t
+        kind = "port"
+        what = f"oracle/oracle.c (the reference engine restated in C), {cores} threads"
+    rows = _band_rows(img, 0, per_step_s, sample)
+    times = []
+    for k in range(args.warmup + args.steps):
+        dt = sample(rows)
+        if k >= args.warmup:
+            times.append(dt)
+    value = rows * W * len(times) / sum(times) / 1e6
+    line = {
+        "impl": "reference", "metric": "Mpixel/s per filter/window", "value": round(value, 4),
+        "unit": "Mpixel/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d))",
+        "config": config_dict(config, ws),
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel/s", "cores": cores, "kind": kind,
+                         "sample": f"{what}: each step filters the top {rows} full-width rows ({rows * W} px) of "
+                                   f"the {config} frame; {cpu_info()['cpu_model']}"},
+        "e2e": {"value": round(value, 4), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU side --
+
+def _host_loop(fn, min_calls: int, warm_s: float = 0.5, reps: int = 5):
+    """Median over `reps` timed loops of `min_calls` synchronous calls of fn()
+    (wall clock), after >= warm_s of warm-up calls: the first host-path
+    calls run slow (host clock ramp, pinned-page and driver warm-up)."""
+    t_w = time.perf_counter()
+    n_w = 0
+    while n_w < 3 or time.perf_counter() - t_w < warm_s:
+        fn()
+        n_w += 1
+    loops = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for _ in range(min_calls):
+            fn()
+        loops.append((time.perf_counter() - t0) / min_calls)
+    return float(np.median(loops)), loops
+
+
+def time_steps(torch, step, steps, flush, cover=True):
+    """CUDA-event device time (ms) of each of ``steps`` calls of step(), an L2
+    flush before each (outside the events); a device sleep between flush and
+    start event keeps the host launch path off the measured interval.  Two
+    untimed passes of the exact timed body run first."""
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    for k in range(-2, steps):
+        flush.fill_(k & 0xff)
+        if cover:
+            torch.cuda._sleep(80000)
+        if k >= 0:
+            starts[k].record()
+        step()
+        if k >= 0:
+            ends[k].record()
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)]
+
+
+def redecided_count(torch, step, ws_buf):
+    """Float64 re-decisions of one step (diagnostic counters)."""
+    import ctypes
+
+    from paper_1009_0958_b200 import _lib
+
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib().dfg_reset_counts(ctypes.c_void_p(ws_buf.data_ptr()), None))
+    step()
+    torch.cuda.synchronize()
+    cnt = ctypes.c_int64(0)
+    _lib.check(_lib.lib().dfg_fixup_count(ctypes.c_void_p(ws_buf.data_ptr()), None, ctypes.byref(cnt)))
+    return int(cnt.value)
+
+
+def roofline_of(config, px_per_s_gpu, world):
+    peak_fma, hbm_peak, sm_mhz, peak_src = peaks()
+    fma_px, mufu_px = WORK[config]
+    achieved = px_per_s_gpu * fma_px / 1e12
+    traffic, traffic_src, pipes = None, None, None
+    if world == 1:  # DRAM bytes per launch of this config's kernel, from the latest ncu --set full capture
+        for tf in sorted(ROOT.glob("profiles/r*_traffic.json"), reverse=True):
+            try:
+                t = json.loads(tf.read_text()).get(config)
+            except (OSError, ValueError):
+                t = None
+            if t:
+                traffic, traffic_src = int(t["dram_bytes"]), f"{tf.relative_to(ROOT)}: {t['kernel'][:60]}"
+                pipes = {k: round(t[k], 1) for k in ("fma_pipe_cycles_active_pct", "fma_pipe_inst_pct",
+                                                     "xu_pipe_inst_pct", "issue_active_pct") if k in t}
+                break
+    return {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak_fma / 1e12, 3),
+            "unit": "T FMA-pipe lane-ops/s", "frac": round(achieved * 1e12 / peak_fma, 4), "traffic": traffic,
+            "traffic_note": (f"dram read+write bytes per launch (ncu, {traffic_src})" if traffic else None),
+            "per_px": {"fma": fma_px, "mufu": mufu_px},
+            "ncu_issue": ({**pipes, "note": "measured FP32 (FMA pipe) / SFU (XU) issue utilisation of this config's "
+                           "kernel in the round's ncu capture; frac above credits only the canonical paper-formula "
+                           "work (SURVEY 8(d))"} if pipes else None),
+            "note": "SURVEY 8(d) canonical FMA-pipe work per pixel x device px/s per GPU; peak = 148 SM x 128 lanes x "
+                    f"{sm_mhz:.0f} MHz ({peak_src})",
+            "hbm": {"achieved": round(px_per_s_gpu * BYTES_PER_PX / 1e9, 2), "peak": hbm_peak, "unit": "GB/s",
+                    "frac": round(px_per_s_gpu * BYTES_PER_PX / 1e9 / hbm_peak, 5)}}
 
 
 def c4_quality(config, spec, x, out, F, torch):
-    """C4 asks for the accelerated variants' PSNR / MAE deltas versus the exact
-    filter (reference metrics.py:64-118), against the clean image the noisy
-    input was made from; computed by the device metrics reduction
-    (dfg_image_metrics), outside the timed region."""
+    """C4's accelerated variants: PSNR / MAE / NCD deltas versus the exact
+    filter (reference metrics.py:64-118) against the clean image, by the
+    device metrics reduction, outside the timed region."""
     from paper_1009_0958_b200.metrics import metrics_device
-    from paper_1009_0958_b200.spec import FilterSpec, DirectionalStrategy
+    from paper_1009_0958_b200.spec import DirectionalStrategy, FilterSpec
 
     cfg = synth.CONFIGS[config]
     H, W = cfg["shape"]
@@ -229,129 +490,183 @@ def c4_quality(config, spec, x, out, F, torch):
             "noisy_input": {"mae": round(mae_n, 4), "psnr_db": round(psnr_n, 4), "ncd_x1000": round(ncd_n, 4)}}
 
 
-def run_reference(args, config):
-    """--impl reference: the reference algorithm on the host cores."""
-    ws, rank, _ = dist_env()
-    if rank != 0:
-        return
-    cfg = synth.CONFIGS[config]
-    spec = parse_filter_spec(cfg["spec"])
-    img = synth.config_input(config, frames=1)
-    if img.ndim == 4:
-        img = img[0]
-    H, W = img.shape[:2]
-    threads = os.cpu_count() or 1
-    # size each step so the whole --steps/--warmup run stays within ~2 minutes
-    per_step_s = max(0.5, min(10.0, 120.0 / (args.steps + args.warmup)))
-    rows = cpu_rows_for(img, spec, per_step_s, threads)
-    times = []
-    for k in range(args.warmup + args.steps):
-        r0 = (k * rows) % max(1, H - rows + 1)
-        dt = oracle_band(img, spec, r0, rows, threads)
-        if k >= args.warmup:
-            times.append(dt)
-    px = rows * W
-    value = px * len(times) / sum(times) / 1e6
-    line = {
-        "impl": "reference", "metric": "Mpixel/s per filter/window", "value": round(value, 4),
-        "unit": "Mpixel/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(1e3 * sum(times) / len(times), 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, SURVEY 8(d))",
-        "config": {"workload": config, "spec": cfg["spec"], "shape": list(cfg["shape"]),
-                   "sample_rows_per_step": rows},
-        "cpu_baseline": {"value": round(value, 4), "unit": "Mpixel/s", "cores": threads, "kind": "port",
-                         "sample": f"{rows} full-width rows x {W} px of the {config} frame per step "
-                                   f"(oracle/oracle.c: the reference engine restated in C, glibc acos)"},
-        "e2e": {"value": round(value, 4), "unit": "Mpixel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+def e2e_single(wl, spec, F, torch, args, full=True):
+    """N = 1, end to end through the public host APIs (outside the device
+    timing; every call synchronous, inputs in and results back through host
+    memory inside the timed region):
+    * value: the C ABI's host call -- ``filter_host`` (dfg_filter_host:
+      pinned uint8 buffers, banded H2D / kernels / D2H, CUDA graph) once per
+      image; for the C5b batch ``filter_host_frames`` over its 64 frames;
+    * apply_filter: the drop-in ``apply_filter`` with a float64 RasterImage
+      in and out (dfg_filter_host_f64: validation + conversion on the host
+      cores, pinned staging);
+    * frame_stream: ``filter_host_frames`` over a stream of frames."""
+    from paper_1009_0958_b200 import RasterImage, apply_filter
 
-
-FRAME_SLOTS = int(os.environ.get("DFG_FRAME_SLOTS", "4"))  # device slots of dfg_filter_host_frames (csrc/dfg_api.cu frame_slots())
-
-
-def _host_loop(fn, min_calls: int, warm_s: float = 0.5, reps: int = 5):
-    """Median over `reps` timed loops of `min_calls` calls of fn() (wall
-    clock; each call is synchronous), after >= warm_s of warm-up calls: the
-    first few hundred host-path calls run slow (host CPU clock ramp,
-    pinned-page and driver copy-path warm-up; measured 380 -> 150 us/call)."""
-    t_w = time.perf_counter()
-    n_w = 0
-    while n_w < 3 or time.perf_counter() - t_w < warm_s:
-        fn()
-        n_w += 1
-    loops = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        for _ in range(min_calls):
-            fn()
-        loops.append((time.perf_counter() - t0) / min_calls)
-    return float(np.median(loops)), loops
-
-
-def measure_e2e(wl, spec, F, torch, args, world, cdev, dist):
-    """The same metric end to end through the public host API, inputs in and
-    results back through pinned host memory inside the timed region:
-    * value: a stream of frames (``filter_host_frames``, C ABI
-      ``dfg_filter_host_frames``): frame f's H2D overlaps frame f-1's kernel
-      and frame f-2's D2H;
-    * sync_call: one synchronous ``filter_host`` call per step (the
-      drop-in ``apply_filter`` shape; row-band pipeline inside the call)."""
-    if wl["kind"] == "rows":
-        return None
     frames = wl["x"] if wl["kind"] == "batch" else wl["x"][None]
     nf, fb = frames.shape[0], frames[0].nbytes
-    # a ring of distinct pinned buffers (a multiple of the 3 device slots, so
-    # frames sharing a host buffer also share a slot stream)
-    ring = nf if wl["kind"] == "batch" else (2 * FRAME_SLOTS if fb < (64 << 20) else FRAME_SLOTS)
-    hin = [torch.from_numpy(frames[i % nf]).pin_memory() for i in range(ring)]
-    hout = [torch.empty(frames.shape[1:], dtype=torch.uint8).pin_memory() for _ in range(ring)]
-    ins, outs = [t.numpy() for t in hin], [t.numpy() for t in hout]
-    if wl["kind"] == "batch":
-        n_frames, calls = nf, max(1, min(args.steps, 3))
-    else:
-        n_frames = max(args.steps, int(min(120, max(12, 0.05 / max(fb / 40e9, 1e-6)))))
-        n_frames = (n_frames + ring - 1) // ring * ring
-        calls = 1
-    seq_in = [ins[f % ring] for f in range(n_frames)]
-    seq_out = [outs[f % ring] for f in range(n_frames)]
-    if world > 1:
-        dist.barrier()
-    s_frames, loops = _host_loop(lambda: F.filter_host_frames(seq_in, spec, out=seq_out), calls, warm_s=0.5, reps=5)
     px_frame = int(np.prod(frames.shape[1:3]))
-    # check the streamed results once (every frame equals the device path's)
+    hin = [torch.from_numpy(frames[i]).pin_memory() for i in range(nf)]
+    hout = [torch.empty(frames.shape[1:], dtype=torch.uint8).pin_memory() for _ in range(nf)]
+    ins, outs = [t.numpy() for t in hin], [t.numpy() for t in hout]
+    big = px_frame * nf > (16 << 20)
+    reps = 3 if big else 5
+    if wl["kind"] == "batch":
+        s_step, _ = _host_loop(lambda: F.filter_host_frames(ins, spec, out=outs), 1, warm_s=0.3, reps=reps)
+        path = (f"filter_host_frames (C ABI dfg_filter_host_frames) over the {nf} frames: H2D + kernel + D2H of "
+                f"every frame inside, up to 4 frames in flight; median of {reps} calls")
+    else:
+        calls = 1 if big else max(3, min(100, int(0.03 / max(fb / 20e9, 1e-6))))
+        s_step, _ = _host_loop(lambda: F.filter_host(ins[0], spec, out=outs[0]), calls, warm_s=0.3, reps=reps)
+        path = ("filter_host (C ABI dfg_filter_host): one synchronous call per image, pinned uint8 host buffers, "
+                f"row-band pipeline (H2D / band kernels / D2H overlapped) replayed as a CUDA graph; median of {reps} "
+                "timed loops")
     dev = torch.device("cuda", torch.cuda.current_device())
     ref = F.filter_device(torch.from_numpy(frames[0]).to(dev), spec).cpu().numpy()
-    assert (outs[0] == ref).all(), "frame stream result differs from the device path"
-    sync = None
-    if wl["kind"] == "image":
-        a_in, a_out = ins[0], outs[0]
-        per_frame = s_frames / n_frames
-        n_calls = max(3, min(max(args.steps, 100), int(0.03 / per_frame)))
-        s_call, _ = _host_loop(lambda: F.filter_host(a_in, spec, out=a_out), n_calls, warm_s=0.5, reps=5)
-        sync = s_call
-    et = torch.tensor([s_frames, sync or 0.0], dtype=torch.float64, device=cdev)
-    if world > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    s_frames, sync = float(et[0].item()), (float(et[1].item()) or None)
-    e_ms = s_frames * 1e3 * (1 if wl["kind"] == "batch" else 1.0 / n_frames)  # per step (one image / one batch)
-    out = {"value": round(wl["total_px"] / (e_ms / 1e3) / 1e6, 3), "unit": "Mpixel/s",
-           "h2d_bytes_per_step": fb * (nf if wl["kind"] == "batch" else 1),
-           "d2h_bytes_per_step": fb * (nf if wl["kind"] == "batch" else 1), "ms_per_step": round(e_ms, 4),
-           "path": (f"filter_host_frames (C ABI dfg_filter_host_frames): {n_frames} frames per call from a ring of "
-                    f"{ring} pinned host buffers, H2D + kernel + D2H of every frame inside, up to {FRAME_SLOTS} frames in "
-                    "flight; median of 5 timed calls"
-                    if wl["kind"] == "image" else
-                    f"filter_host_frames over the {nf} frames of the batch, H2D + kernel + D2H of every frame "
-                    f"inside, up to {FRAME_SLOTS} frames in flight; median of 5 timed calls")}
-    if sync:
-        out["sync_call"] = {"value": round(px_frame * world / sync / 1e6, 3), "unit": "Mpixel/s",
-                            "ms_per_step": round(sync * 1e3, 4),
-                            "path": "filter_host (C ABI dfg_filter_host): one synchronous call per image, row-band "
-                                    "pipeline + CUDA graph inside; median of 5 timed loops"}
-    if os.environ.get("BENCH_E2E_DEBUG"):
-        print("e2e frame-stream loops (ms/call): " + " ".join(f"{x * 1e3:.3f}" for x in loops), file=sys.stderr)
+    assert (outs[0] == ref).all(), "host path result differs from the device path"
+    total_px = px_frame * nf
+    out = {"value": round(total_px / s_step / 1e6, 3), "unit": "Mpixel/s", "h2d_bytes_per_step": fb * nf,
+           "d2h_bytes_per_step": fb * nf, "ms_per_step": round(s_step * 1e3, 4), "path": path}
+    if not full:
+        return out
+    # the drop-in: float64 RasterImage in, new float64 RasterImage out
+    img64 = RasterImage(frames[0].astype(np.float64))
+    s_af, _ = _host_loop(lambda: apply_filter(img64, spec), 1, warm_s=0.2, reps=3)
+    out["apply_filter"] = {"value": round(px_frame / s_af / 1e6, 3), "unit": "Mpixel/s",
+                           "ms_per_step": round(s_af * 1e3, 3), "h2d_bytes_per_step": fb, "d2h_bytes_per_step": fb,
+                           "host_bytes_per_step": 2 * 8 * px_frame * 3,
+                           "path": "apply_filter(RasterImage float64) -> RasterImage float64 (C ABI "
+                                   "dfg_filter_host_f64: integrality/range check + conversion on all host cores "
+                                   "into pinned staging, then the dfg_filter_host pipeline; output array "
+                                   "allocated per call, as the reference does); median of 3 calls"}
+    if wl["kind"] == "image" and not big:
+        ring = 8
+        seq_in = [ins[0]] * 120
+        outs_ring = [torch.empty(frames.shape[1:], dtype=torch.uint8).pin_memory().numpy() for _ in range(ring)]
+        seq_out = [outs_ring[f % ring] for f in range(120)]
+        s_fs, _ = _host_loop(lambda: F.filter_host_frames(seq_in, spec, out=seq_out), 1, warm_s=0.3, reps=5)
+        out["frame_stream"] = {"value": round(120 * px_frame / s_fs / 1e6, 3), "unit": "Mpixel/s",
+                               "path": "filter_host_frames: 120 frames per call, up to 4 in flight"}
     return out
+
+
+def measure_config(config, args, torch, F, dist, world, rank, dev, cdev, flush, *, headline: bool):
+    """Device timing (+ for N = 1 and rank 0: e2e, parity, CPU baseline) of
+    one config.  Returns the JSON fields."""
+    from paper_1009_0958_b200 import _lib
+    from paper_1009_0958_b200.parallel import StripJob
+
+    cfg = synth.CONFIGS[config]
+    spec = parse_filter_spec(cfg["spec"])
+    wl = workload(config, rank, world)
+    ws_buf = torch.zeros(_lib.lib().dfg_workspace_bytes(1), dtype=torch.uint8, device=dev)
+    steps = args.steps if headline else max(5, min(args.steps, 20))
+    extra = {}
+    if wl["kind"] == "strips":
+        jobs = {}
+        for mode in ("gather", "resident"):
+            job = StripJob(wl["H"], wl["W"], spec.window, gather=(mode == "gather"), chunks=args.chunks, device=dev)
+            job.own.copy_(torch.from_numpy(wl["x"][job.r0:job.r1]))
+            jobs[mode] = job
+
+        def fn(strip, H, i0, a, n, out):
+            F.filter_rows_device(strip, H, i0, a, n, spec, out=out, ws=ws_buf)
+
+        chunks_mine = sum(1 for a, b in jobs["gather"]._chunk_bounds(rank) if b > a)
+
+        def step():
+            jobs["gather"].run(fn)
+
+        def step_res():
+            jobs["resident"].run(fn)
+        out_t = jobs["gather"].out
+        px_rank = (jobs["gather"].r1 - jobs["gather"].r0) * wl["W"]
+        launches = chunks_mine
+    else:
+        x = torch.from_numpy(wl["x"]).to(dev)
+        out_t = torch.empty_like(x)
+        if wl["kind"] == "batch":
+            def step():
+                F.filter_batch_device(x, spec, out=out_t, ws=ws_buf)
+        else:
+            def step():
+                F.filter_device(x, spec, out=out_t, ws=ws_buf)
+        px_rank = wl["px"]
+        launches = 1
+    for _ in range(args.warmup):
+        step()
+    redecided = redecided_count(torch, step, ws_buf)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(dev.index) if headline else None
+    if clk:
+        clk.__enter__()
+    ms = time_steps(torch, step, steps, flush)
+    if clk:
+        clk.__exit__(None, None, None)
+    if wl["kind"] == "strips":
+        ms_res = time_steps(torch, step_res, steps, flush)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tot = torch.tensor([sum(ms), sum(ms_res) if wl["kind"] == "strips" else 0.0], dtype=torch.float64, device=cdev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    ms_step = float(tot[0].item()) / steps
+    value = wl["total_px"] / (ms_step / 1e3) / 1e6
+    res = {"value": round(value, 3), "ms_per_step": round(ms_step, 5), "steps": steps,
+           "scaling": wl["scaling"], "redecided_px_per_step": redecided, "gpu_launches": launches * steps,
+           "roofline": roofline_of(config, px_rank / (ms_step / 1e3), world)}
+    if wl["kind"] == "strips":
+        ms_r = float(tot[1].item()) / steps
+        res["resident_output"] = {"value": round(wl["total_px"] / (ms_r / 1e3) / 1e6, 3),
+                                  "ms_per_step": round(ms_r, 5),
+                                  "note": "same step without the gather: filtered rows stay on their rank"}
+        res["step"] = (f"NCCL halo exchange (s//2 rows per neighbour) + {args.chunks} row chunks of "
+                       "dfg_filter_rows per rank + chunk-by-chunk gather to rank 0 (parallel.StripJob)")
+    if clk:
+        res["clocks"] = clk.summary()
+    # e2e (N > 1: C5a strips -- own rows H2D from pinned host memory, the
+    # step, the gathered frame D2H on the root -- device-timed, max over ranks)
+    if world > 1:
+        if wl["kind"] == "strips":
+            job = jobs["gather"]
+            h_own = torch.from_numpy(np.ascontiguousarray(wl["x"][job.r0:job.r1])).pin_memory()
+            h_out = torch.empty(tuple(job.out.shape), dtype=torch.uint8).pin_memory()
+
+            def e2e_step():
+                job.own.copy_(h_own, non_blocking=True)
+                job.run(fn)
+                if rank == 0:
+                    h_out.copy_(job.out, non_blocking=True)
+            ems = time_steps(torch, e2e_step, max(3, min(steps, 10)), flush)
+            et = torch.tensor([sum(ems) / len(ems)], dtype=torch.float64, device=cdev)
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+            e_ms = float(et.item())
+            res["e2e"] = {"value": round(wl["total_px"] / (e_ms / 1e3) / 1e6, 3), "unit": "Mpixel/s",
+                          "ms_per_step": round(e_ms, 4), "h2d_bytes_per_step": int(h_own.numel()),
+                          "d2h_bytes_per_step": int(h_out.numel()) if rank == 0 else 0,
+                          "path": "each rank's own rows H2D from pinned host memory + the strip step + the gathered "
+                                  "frame D2H on rank 0; CUDA events, max over ranks"}
+        return res
+    if rank != 0:
+        return res
+    res["e2e"] = e2e_single(wl, spec, F, torch, args, full=headline)
+    if config.startswith("c4_"):
+        res["quality"] = c4_quality(config, spec, torch.from_numpy(wl["x"]).to(dev), out_t, F, torch)
+    img0 = wl["x"][0] if wl["x"].ndim == 4 else wl["x"]
+    if not args.no_cpu:
+        res["cpu_baseline"] = cpu_baseline(img0, cfg["spec"], args.cpu_seconds if headline else 3.0, full=headline)
+    if not args.no_parity:
+        import oracle  # the checker (test infrastructure), outside every timed region
+
+        t0 = time.perf_counter()
+        rep = oracle.parity_report(out_t.cpu().numpy(), wl["x"], spec)
+        rep["checker"] = "oracle/oracle.c float64, every output pixel"
+        rep["seconds"] = round(time.perf_counter() - t0, 1)
+        res["parity"] = rep
+    return res
 
 
 def run_ours(args, config):
@@ -361,166 +676,74 @@ def run_ours(args, config):
     from paper_1009_0958_b200 import filters as F
 
     world, rank, local = dist_env()
-    local = local % max(1, torch.cuda.device_count())  # (ranks sharing a GPU: gloo smoke runs only)
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    backend = args.dist_backend
     if world > 1:
-        if backend == "nccl":
+        if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
-            dist.init_process_group(backend)
-    cdev = dev if backend == "nccl" else torch.device("cpu")  # where the timing reductions live
-    cfg = synth.CONFIGS[config]
-    spec = parse_filter_spec(cfg["spec"])
-    wl = workload(config, rank, world)
-    x = torch.from_numpy(wl["x"]).to(dev)
-    out = torch.empty_like(x) if wl["kind"] != "rows" else torch.empty((wl["out_rows"],) + tuple(x.shape[1:]),
-                                                                       dtype=torch.uint8, device=dev)
-    from paper_1009_0958_b200 import _lib
-
-    ws_buf = torch.zeros(_lib.lib().dfg_workspace_bytes(wl["px"]), dtype=torch.uint8, device=dev)
+            dist.init_process_group(args.dist_backend)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
-    def step():
-        if wl["kind"] == "image":
-            F.filter_device(x, spec, out=out, ws=ws_buf)
-        elif wl["kind"] == "batch":
-            F.filter_batch_device(x, spec, out=out, ws=ws_buf)
-        else:
-            F.filter_rows_device(x, wl["H"], wl["in_row0"], wl["out_row0"], wl["out_rows"], spec, out=out, ws=ws_buf)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    import ctypes
-
-    # float64 re-decisions of one step (diagnostic counters, outside the timing)
-    _lib.check(_lib.lib().dfg_reset_counts(ctypes.c_void_p(ws_buf.data_ptr()), None))
-    step()
-    torch.cuda.synchronize()
-    cnt = ctypes.c_int64(0)
-    _lib.check(_lib.lib().dfg_fixup_count(ctypes.c_void_p(ws_buf.data_ptr()), None, ctypes.byref(cnt)))
-    redecided = int(cnt.value)
-
-    # launch cover: a ~40 us device-side sleep between the L2 flush and each
-    # start event, so the host's Python/ctypes launch path (tens of us) runs
-    # while the GPU is still busy and the events bracket the kernel itself,
-    # not the host launch latency (the role the SURVEY 8(d) graph capture of
-    # C1/C2 plays; a graph cannot interleave the per-step L2 flush)
-    cover_cycles = 0 if os.environ.get("BENCH_NO_COVER") else 80000
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        # two untimed passes of the exact timed body first: the first pass of
-        # flush + sleep + events + kernel measured 4x a steady step (C1: 85-104
-        # vs 22.5 us), which at 20 steps inflated C1's mean by ~15 %
-        for k in range(-2, args.steps):
-            flush.fill_(k & 0xff)
-            if cover_cycles:
-                torch.cuda._sleep(cover_cycles)  # the step's launch is queued before its start event fires
-            if k >= 0:
-                starts[k].record()
-            step()
-            if k >= 0:
-                ends[k].record()
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    if os.environ.get("BENCH_STEP_DEBUG"):
-        print("step ms: " + " ".join(f"{x:.4f}" for x in ms), file=sys.stderr)
-    tot = torch.tensor([sum(ms)], dtype=torch.float64, device=cdev)
-    if world > 1:
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    tot_ms = float(tot.item())
-    ms_step = tot_ms / args.steps
-    value = wl["total_px"] / (ms_step / 1e3) / 1e6  # Mpixel/s, whole job
-
-    # end to end through the C ABI's host paths (pinned host buffers, H2D + D2H inside)
-    e2e = measure_e2e(wl, spec, F, torch, args, world, cdev, dist)
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
-    quality = c4_quality(config, spec, x, out, F, torch) if config.startswith("c4_") else None
-    peak_fma, hbm_peak, sm_mhz, peak_src = peaks()
-    fma_px, mufu_px = WORK[config]
-    px_per_s_gpu = wl["px"] / (ms_step / 1e3)
-    achieved = px_per_s_gpu * fma_px / 1e12
-    traffic, traffic_src, pipes = None, None, None
-    if world == 1:  # DRAM bytes per launch of this config's kernel, from the round's ncu --set full capture
-        for tf in sorted(ROOT.glob("profiles/r*_traffic.json"), reverse=True):
-            try:
-                t = json.loads(tf.read_text()).get(config)
-            except (OSError, ValueError):
-                t = None
-            if t:
-                traffic, traffic_src = int(t["dram_bytes"]), f"{tf.relative_to(ROOT)}: {t['kernel'][:60]}"
-                pipes = {k: round(t[k], 1) for k in ("fma_pipe_cycles_active_pct", "fma_pipe_inst_pct",
-                                                     "xu_pipe_inst_pct", "issue_active_pct") if k in t}
-                break
-    roofline = {"bound": "fp32", "achieved": round(achieved, 3), "peak": round(peak_fma / 1e12, 3),
-                "unit": "T FMA-pipe lane-ops/s", "frac": round(achieved * 1e12 / peak_fma, 4), "traffic": traffic,
-                "traffic_note": (f"dram read+write bytes per launch (ncu, {traffic_src}); algorithmic "
-                                 f"{BYTES_PER_PX * wl['px']} B per launch") if traffic else None,
-                "per_px": {"fma": fma_px, "mufu": mufu_px},
-                "ncu_issue": ({**pipes, "note": "measured FP32 (FMA pipe) / SFU (XU) issue utilisation of this "
-                               "config's kernel in the round's ncu capture -- the north star's 'achieved FP32/SFU "
-                               "issue rate against peak'; frac above credits only the canonical paper-formula work"}
-                              if pipes else None),
-                "note": "SURVEY 8(d) canonical work per pixel / device time of the step's single kernel (FP32 "
-                        f"decision + in-kernel float64 re-decision); peak = 148 SM x 128 lanes x {sm_mhz:.0f} MHz "
-                        f"({peak_src})",
-                "hbm": {"achieved": round(px_per_s_gpu * BYTES_PER_PX / 1e9, 2), "peak": hbm_peak, "unit": "GB/s",
-                        "frac": round(px_per_s_gpu * BYTES_PER_PX / 1e9 / hbm_peak, 5)}}
-    # CPU baseline: the oracle on a bounded sample of the same workload
-    cpu = None
-    if world == 1 and not args.no_cpu:
-        img = wl["x"][0] if wl["x"].ndim == 4 else wl["x"]
-        threads = os.cpu_count() or 1
-        rate, rows, passes, dt = cpu_rate(img, spec, args.cpu_seconds, threads)
-        cpu = {"value": round(rate, 4), "unit": "Mpixel/s", "cores": threads, "kind": "port",
-               "sample": f"{passes} passes over {rows} full-width rows ({rows * img.shape[1]} px) of the {config} "
-                         f"frame, {dt:.1f} s of CPU work, oracle/oracle.c (reference engine restated in C, "
-                         "float64, glibc acos)"}
-    launches = args.steps  # one decision kernel per step (float64 re-decision runs inside it)
-    line = {
-        "metric": "Mpixel/s per filter/window", "value": round(value, 3), "unit": "Mpixel/s",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
-        "higher_is_better": True, "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f32+f64 (u8 io)",
-        "data": "synthetic (seeded gradient + 20 rectangles + impulsive noise, SURVEY 8(d))",
-        "config": {"workload": config, "spec": cfg["spec"], "shape": list(cfg["shape"]),
-                   "noise": list(cfg["noise"]), "seed": cfg["seed"], "frames": cfg.get("frames", 1),
-                   "l2": "flushed between timed steps (256 MiB write)", "launch": ("host launch hidden behind a device sleep before each start event" if not os.environ.get("BENCH_NO_COVER") else "uncovered"), "parallelism": f"{wl['kind']} x{world}"},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-        "redecided_px_per_step": redecided, "clocks": clk.summary(),
-        **({"quality": quality} if quality else {}),
-    }
-    print(json.dumps(line), flush=True)
+    head = measure_config(config, args, torch, F, dist, world, rank, dev, cdev, flush, headline=True)
+    table = None
+    if world == 1 and not args.no_table:
+        table = {}
+        for c in synth.CONFIGS:
+            if c == config:
+                continue
+            r = measure_config(c, args, torch, F, dist, 1, 0, dev, cdev, flush, headline=False)
+            r["frac"] = r["roofline"]["frac"]
+            r["roofline"] = {k: r["roofline"][k] for k in ("frac", "achieved", "peak", "unit", "traffic")}
+            table[c] = r
+            torch.cuda.empty_cache()
+    if rank == 0:
+        line = {
+            "metric": "Mpixel/s per filter/window", "value": head["value"], "unit": "Mpixel/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": head["scaling"], "vs_baseline": None, "dtype": "f32+f64 (u8 io)",
+            "data": "synthetic (seeded gradient + 20 rectangles + impulsive noise, SURVEY 8(d))",
+            "config": config_dict(config, world),
+            "roofline": head["roofline"], "cpu_baseline": head.get("cpu_baseline"), "e2e": head.get("e2e"),
+            "parity": head.get("parity"), "gpu_launches": head["gpu_launches"],
+            "redecided_px_per_step": head["redecided_px_per_step"], "clocks": head.get("clocks"),
+        }
+        for k in ("resident_output", "step", "quality"):
+            if k in head:
+                line[k] = head[k]
+        if table is not None:
+            line["configs"] = table
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def workload_kind(config, world):
+    if config == "c5b":
+        return "batch"
+    return "strips" if (config == "c5a" and world > 1) else "image"
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--dist-backend", default="nccl", choices=("nccl", "gloo"),
                     help="process-group backend for the timing barrier/max (gloo only for smoke runs)")
-    ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(synth.CONFIGS))
+    ap.add_argument("--chunks", type=int, default=4, help="row chunks per strip (C5a, N > 1)")
+    ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-table", action="store_true", help="skip the per-config table")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     if args.impl == "reference":
         run_reference(args, args.config)
     else:

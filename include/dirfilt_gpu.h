@@ -100,11 +100,9 @@ typedef struct dfg_params {
 DFG_API int dfg_abi_version(void);
 DFG_API const char *dfg_last_error(void);
 
-/* Device workspace needed to filter up to n_pixels output pixels per call:
- * diagnostic counters and the 3x3 row sweep's deferred float64 re-decision
- * queue.  Zero it once after allocation (every call leaves its queue state
- * reset).  A workspace serves one call at a time: calls that may run
- * concurrently (different streams) need separate workspaces. */
+/* Device workspace of a filter call (n_pixels output pixels): the diagnostic
+ * counters of dfg_fixup_count.  Zero it once after allocation; calls only
+ * add to the counters, so calls on different streams may share it. */
 DFG_API size_t dfg_workspace_bytes(int64_t n_pixels);
 
 /* Whole image: d_in (H, W, 3) -> d_out (H, W, 3), both device memory. */
@@ -138,6 +136,17 @@ DFG_API int dfg_filter_batch(const uint8_t *d_in, int32_t B, int32_t H, int32_t 
 DFG_API int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out,
                     const dfg_params *prm, void *stream);
 
+/* The reference's own boundary (RasterImage pixels: C-contiguous float64
+ * (H, W, 3), image.py:65-75) end to end from HOST memory: the values are
+ * validated and converted to uint8 on `threads` host threads (0: all cores)
+ * into cached pinned staging buffers, filtered by the dfg_filter_host
+ * pipeline, and written back to h_out as float64.  Values that are not
+ * integers in 0..255 (incl. NaN/inf) return DFG_E_ARG -- the GPU path's one
+ * restriction against the reference, which accepts any finite nonnegative
+ * float64. */
+DFG_API int dfg_filter_host_f64(const double *h_in, int32_t H, int32_t W, double *h_out,
+                    const dfg_params *prm, int32_t threads, void *stream);
+
 /* A stream of n independent (H, W, 3) frames from HOST memory (one buffer
  * per frame, pinned for overlap), synchronised before return: the
  * reference's per-frame apply_filter loop (bench.py:96-109, cli filter over
@@ -147,6 +156,22 @@ DFG_API int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *
 DFG_API int dfg_filter_host_frames(const uint8_t *const *h_in, uint8_t *const *h_out,
                     int32_t n_frames, int32_t H, int32_t W,
                     const dfg_params *prm, void *stream);
+
+/* Schedule / diagnostic options (process-wide; for tests and measurement
+ * scripts -- the library reads no environment variables).  Defaults are the
+ * production settings. */
+#define DFG_OPT_S3_SCHEDULE 1   /* 3x3 schedule: 0 auto, 1 warp row sweep, 2 CTA tiles */
+#define DFG_OPT_NO_FIXUP 2      /* 1: skip the float64 re-decision (timing only; results may differ) */
+#define DFG_OPT_HOST_BANDS 3    /* dfg_filter_host row bands: 0 auto */
+#define DFG_OPT_HOST_GRAPH 4    /* dfg_filter_host: replay pinned pipelines as CUDA graphs (default 1) */
+#define DFG_OPT_HOST_W3_RPC 5   /* rows per chunk of the host pipeline's 3x3 band kernels (default 8) */
+#define DFG_OPT_FRAME_SLOTS 6   /* dfg_filter_host_frames device slots, 1..8 (default 4) */
+#define DFG_OPT_W3_WPS 7        /* 3x3 row sweep: resident warps per SM its chunking targets (0 auto) */
+#define DFG_OPT_W3_RPC 8        /* 3x3 row sweep: rows per chunk (0 auto) */
+#define DFG_OPT_W3_SMALL_WPS 9  /* 3x3 row sweep: warps per SM for single-wave frames (default 12) */
+#define DFG_OPT_CR_MARGIN 10    /* relative margin below which the correctly rounded arccos pass runs */
+DFG_API int dfg_set_option(int32_t key, double value);
+DFG_API double dfg_get_option(int32_t key);
 
 /* Pixels re-decided in float64 by the calls on this workspace since the last
  * dfg_reset_counts (synchronous read of the workspace counter; the filter
@@ -209,6 +234,10 @@ DFG_API size_t dfg_calib_scratch_bytes(void);
 DFG_API int dfg_calib_reduce(const dfg_calib_params *cp, int32_t mode, double x0, double x1, double *out3,
                      void *d_scratch, size_t scratch_bytes, void *stream);
 DFG_API int dfg_calib_samples(const dfg_calib_params *cp, double *d_b, double *d_a, void *stream);
+/* The same three reductions (modes 0-2) over n stored device samples
+ * (d_b, d_a) -- reference fit_line, calibration.py:47-80. */
+DFG_API int dfg_moments_reduce(const double *d_b, const double *d_a, int64_t n, int32_t mode, double x0, double x1,
+                     double *out3, void *d_scratch, size_t scratch_bytes, void *stream);
 
 #ifdef __cplusplus
 }

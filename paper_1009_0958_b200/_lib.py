@@ -19,9 +19,10 @@ BORDER_CODE = {"replicate": 0, "reflect": 1}
 # every symbol include/dirfilt_gpu.h declares
 EXPORTS = (
     "dfg_abi_version", "dfg_last_error", "dfg_workspace_bytes", "dfg_filter",
-    "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_filter_host_frames", "dfg_fixup_count",
+    "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_filter_host_f64", "dfg_filter_host_frames",
+    "dfg_set_option", "dfg_get_option", "dfg_fixup_count",
     "dfg_reset_counts", "dfg_debug_values", "dfg_cr_acos_host", "dfg_corrupt_image",
-    "dfg_image_metrics", "dfg_calib_scratch_bytes", "dfg_calib_reduce", "dfg_calib_samples",
+    "dfg_image_metrics", "dfg_calib_scratch_bytes", "dfg_calib_reduce", "dfg_calib_samples", "dfg_moments_reduce",
 )
 
 
@@ -90,7 +91,11 @@ def lib() -> ctypes.CDLL:
     L.dfg_filter_rows.argtypes = [vp, i32, i32, i32, i32, i64, vp, i32, i32, i64, P, vp, sz, vp]
     L.dfg_filter_batch.argtypes = [vp, i32, i32, i32, i64, i64, vp, i64, i64, P, vp, sz, vp]
     L.dfg_filter_host.argtypes = [vp, i32, i32, vp, P, vp]
+    L.dfg_filter_host_f64.argtypes = [vp, i32, i32, vp, P, i32, vp]
     L.dfg_filter_host_frames.argtypes = [vp, vp, i32, i32, i32, P, vp]
+    L.dfg_set_option.argtypes = [i32, ctypes.c_double]
+    L.dfg_get_option.argtypes = [i32]
+    L.dfg_get_option.restype = ctypes.c_double
     L.dfg_fixup_count.argtypes = [vp, vp, ctypes.POINTER(i64)]
     L.dfg_reset_counts.argtypes = [vp, vp]
     L.dfg_debug_values.argtypes = [vp, i32, i32, i64, vp, P, vp]
@@ -102,14 +107,45 @@ def lib() -> ctypes.CDLL:
     L.dfg_calib_reduce.argtypes = [ctypes.POINTER(DfgCalibParams), i32, ctypes.c_double, ctypes.c_double,
                                    ctypes.POINTER(ctypes.c_double), vp, sz, vp]
     L.dfg_calib_samples.argtypes = [ctypes.POINTER(DfgCalibParams), vp, vp, vp]
-    for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_filter_host_frames",
+    L.dfg_moments_reduce.argtypes = [vp, vp, i64, i32, ctypes.c_double, ctypes.c_double,
+                                     ctypes.POINTER(ctypes.c_double), vp, sz, vp]
+    for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_filter_host_f64",
+                 "dfg_filter_host_frames", "dfg_set_option",
                  "dfg_fixup_count", "dfg_reset_counts", "dfg_debug_values", "dfg_corrupt_image",
-                 "dfg_image_metrics", "dfg_calib_reduce", "dfg_calib_samples"):
+                 "dfg_image_metrics", "dfg_calib_reduce", "dfg_calib_samples", "dfg_moments_reduce"):
         getattr(L, name).restype = ctypes.c_int
     if L.dfg_abi_version() != 1:
         raise RuntimeError("libdfg.so ABI version mismatch; rebuild")
     _lib = L
     return L
+
+
+# schedule / diagnostic options (DFG_OPT_* in include/dirfilt_gpu.h)
+OPTIONS = {"s3_schedule": 1, "no_fixup": 2, "host_bands": 3, "host_graph": 4, "host_w3_rpc": 5,
+           "frame_slots": 6, "w3_wps": 7, "w3_rpc": 8, "w3_small_wps": 9, "cr_margin": 10}
+
+
+def set_option(name: str, value) -> float:
+    """Set a process-wide library option; returns the previous value."""
+    key = OPTIONS[name]
+    old = lib().dfg_get_option(key)
+    check(lib().dfg_set_option(key, float(value)))
+    return old
+
+
+class option:
+    """Context manager: ``with option("s3_schedule", 2): ...``"""
+
+    def __init__(self, name: str, value):
+        self.name, self.value = name, value
+
+    def __enter__(self):
+        self.old = set_option(self.name, self.value)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, self.old)
+        return False
 
 
 def check(rc: int) -> None:

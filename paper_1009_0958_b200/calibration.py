@@ -124,8 +124,10 @@ def sample_angle_chromaticity_pairs(pairs: int, seed: int, p: float = 2.0, *, de
 
 
 def fit_line(b, a, method: str = "tls") -> LinearFit:
-    """Fit a line to (b, a) samples (reference calibration.py:47-80), moments
-    reduced on the device (float64)."""
+    """Fit a line to (b, a) samples (reference calibration.py:47-80): the
+    means, central second moments and residual sums are three passes of the
+    device reduction kernel (``dfg_moments_reduce``, float64, fixed order);
+    only the line formula's few scalars are evaluated on the host."""
     if method not in ("tls", "ols"):
         raise ValueError(f"unknown regression method {method!r}")
     torch = _torch()
@@ -133,17 +135,31 @@ def fit_line(b, a, method: str = "tls") -> LinearFit:
     ta = torch.as_tensor(np.asarray(a, dtype=np.float64) if not torch.is_tensor(a) else a, dtype=torch.float64)
     if tb.shape != ta.shape or tb.dim() != 1 or tb.numel() < 2:
         raise ValueError("need two equal-length 1-D sample arrays")
-    tb, ta = tb.cuda(), ta.cuda()
-    mb, ma = float(tb.mean()), float(ta.mean())
-    sxx = float(((tb - mb) ** 2).mean())
-    syy = float(((ta - ma) ** 2).mean())
-    sxy = float(((tb - mb) * (ta - ma)).mean())
-    if sxx < 1e-30:
-        raise ValueError("degenerate samples: no variance in B (all pairs parallel?)")
-    slope = _slope(method, sxx, syy, sxy)
-    intercept = ma - slope * mb
-    resid = ta - (slope * tb + intercept)
-    rms = float(torch.sqrt((resid * resid).mean()))
-    return LinearFit(slope=float(slope), intercept=float(intercept), fit_error=rms, sample_count=int(tb.numel()),
-                     mean_abs_residual=float(resid.abs().mean()), rms_orthogonal=rms / math.sqrt(1.0 + slope * slope),
+    dev = tb.device if tb.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    tb, ta = tb.to(dev).contiguous(), ta.to(dev).contiguous()
+    n = int(tb.numel())
+    L = _lib.lib()
+    nbytes = L.dfg_calib_scratch_bytes()
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    out = (ctypes.c_double * 3)()
+    stream = _stream_ptr(torch, None, dev)
+
+    def reduce(mode, x0=0.0, x1=0.0):
+        _lib.check(L.dfg_moments_reduce(ctypes.c_void_p(tb.data_ptr()), ctypes.c_void_p(ta.data_ptr()), n, mode,
+                                        x0, x1, out, ctypes.c_void_p(scratch.data_ptr()), nbytes, stream))
+        return out[0], out[1], out[2]
+
+    with torch.cuda.device(dev):
+        sb, sa, _ = reduce(0)
+        mb, ma = sb / n, sa / n
+        cxx, cyy, cxy = reduce(1, mb, ma)
+        sxx, syy, sxy = cxx / n, cyy / n, cxy / n
+        if sxx < 1e-30:
+            raise ValueError("degenerate samples: no variance in B (all pairs parallel?)")
+        slope = _slope(method, sxx, syy, sxy)
+        intercept = ma - slope * mb
+        r2, rabs, _ = reduce(2, slope, intercept)
+    rms = math.sqrt(r2 / n)
+    return LinearFit(slope=float(slope), intercept=float(intercept), fit_error=rms, sample_count=n,
+                     mean_abs_residual=rabs / n, rms_orthogonal=rms / math.sqrt(1.0 + slope * slope),
                      method=method)

@@ -7,10 +7,37 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include <mutex>
+#include <atomic>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "dfg_internal.cuh"
+
+namespace dfg {
+
+Options &options()
+{
+    static Options o;
+    return o;
+}
+
+int sm_count(int dev)
+{
+    static int cache[64] = {};
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev] == 0) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 148;
+        }
+        cache[dev] = n;
+    }
+    return cache[dev];
+}
+
+}  // namespace dfg
 
 namespace {
 
@@ -29,10 +56,6 @@ int cuda_fail(cudaError_t e, const char *where)
 }
 
 constexpr size_t kWsHeader = 256;
-// deferred float64 re-decision queue of the 3x3 row sweep (16-byte entries
-// after the header): at most this many doubtful pixels per call are queued,
-// the rest are re-decided inline
-constexpr int64_t kQueueCap = 1 << 16;
 
 // Mirrors the reference's validation (filters.py:53-59, 110-123, 141-151,
 // image.py:44-46): invalid -> DFG_E_ARG (ValueError); valid but outside
@@ -110,11 +133,7 @@ void fill_params(const dfg_params *p, dfg::KParams &kp)
     fp.threshold = p->threshold;
     fp.slope = p->slope;
     fp.intercept = p->intercept;
-    static const double cr_margin = [] {
-        const char *e = getenv("DFG_CR_MARGIN");  // diagnostics only
-        return e ? atof(e) : 1e-12;
-    }();
-    fp.cr_margin = cr_margin;
+    fp.cr_margin = dfg::options().cr_margin;
 }
 
 int pcode_of(double p) { return p == 2.0 ? dfg::PC_2 : (p == 1.0 ? dfg::PC_1 : dfg::PC_GEN); }
@@ -145,7 +164,7 @@ cudaError_t launch_fast(const dfg_params *p, cudaStream_t st, const uint8_t *in,
 int run(const uint8_t *d_in, int global_H, int W, int in_row0, int in_rows, long long in_pitch,
         long long in_fstride, uint8_t *d_out, int out_row0, int out_rows, long long out_pitch,
         long long out_fstride, int frames, const dfg_params *prm, void *ws, size_t ws_bytes,
-        void *stream, float *dbg, int w3_rpc = 0, int hostio = 0)
+        void *stream, float *dbg, int w3_rpc = 0)
 {
     int rc = validate(prm);
     if (rc) return rc;
@@ -192,23 +211,8 @@ int run(const uint8_t *d_in, int global_H, int W, int in_row0, int in_rows, long
     fill_params(prm, kp);
     kp.flag_count = (unsigned *)ws;
     kp.dbg = dbg;
-    {
-        const char *dg = getenv("DFG_DIAG_NO_FIXUP");  // diagnostics only
-        kp.diag_no_fixup = (dg && dg[0] == '1') ? 1 : 0;
-        const char *dc = getenv("DFG_DIAG_CYCLES");  // diagnostics only
-        kp.diag_cycles = (dc && dc[0] == '1') ? 1 : 0;
-    }
+    kp.diag_no_fixup = dfg::options().no_fixup;
     kp.w3_rpc = w3_rpc;
-    kp.hostio = hostio;
-    // the deferred queue needs the workspace to itself for the whole launch:
-    // not for the host pipeline's concurrent band kernels (w3_rpc > 0).
-    // Opt-in (DFG_W3_QUEUE=1): measured slower than the inline re-decision
-    // (the drain runs after the sweeps instead of overlapping them)
-    static const bool queue_env = [] {
-        const char *q = getenv("DFG_W3_QUEUE");
-        return q && q[0] == '1';
-    }();
-    kp.w3_queue = (queue_env && w3_rpc == 0 && !hostio) ? (int)(npx < kQueueCap ? npx : kQueueCap) : 0;
 
     cudaError_t e = launch_fast(prm, st, d_in, d_out, kp);
     if (e != cudaSuccess) return cuda_fail(e, "fast kernel launch");
@@ -271,9 +275,47 @@ const char *dfg_last_error(void) { return g_err.c_str(); }
 
 size_t dfg_workspace_bytes(int64_t n_pixels)
 {
-    if (n_pixels < 0) n_pixels = 0;
-    // counters + the 3x3 row sweep's re-decision queue
-    return kWsHeader + 16 * (size_t)(n_pixels < kQueueCap ? n_pixels : kQueueCap);
+    (void)n_pixels;  // diagnostic counters only (the size is kept in the ABI for growth)
+    return kWsHeader;
+}
+
+int dfg_set_option(int32_t key, double value)
+{
+    dfg::Options &o = dfg::options();
+    const int v = (int)value;
+    switch (key) {
+    case DFG_OPT_S3_SCHEDULE: o.s3_schedule = v; break;
+    case DFG_OPT_NO_FIXUP: o.no_fixup = v; break;
+    case DFG_OPT_HOST_BANDS: o.host_bands = v; break;
+    case DFG_OPT_HOST_GRAPH: o.host_graph = v; break;
+    case DFG_OPT_HOST_W3_RPC: o.host_w3_rpc = v; break;
+    case DFG_OPT_FRAME_SLOTS: o.frame_slots = v; break;
+    case DFG_OPT_W3_WPS: o.w3_wps = v; break;
+    case DFG_OPT_W3_RPC: o.w3_rpc = v; break;
+    case DFG_OPT_W3_SMALL_WPS: o.w3_small_wps = v; break;
+    case DFG_OPT_CR_MARGIN: o.cr_margin = value; break;
+    default: return fail(DFG_E_ARG, "unknown option key");
+    }
+    g_host.drop_graphs();  // captured pipelines bake the old settings in
+    return DFG_OK;
+}
+
+double dfg_get_option(int32_t key)
+{
+    const dfg::Options &o = dfg::options();
+    switch (key) {
+    case DFG_OPT_S3_SCHEDULE: return o.s3_schedule;
+    case DFG_OPT_NO_FIXUP: return o.no_fixup;
+    case DFG_OPT_HOST_BANDS: return o.host_bands;
+    case DFG_OPT_HOST_GRAPH: return o.host_graph;
+    case DFG_OPT_HOST_W3_RPC: return o.host_w3_rpc;
+    case DFG_OPT_FRAME_SLOTS: return o.frame_slots;
+    case DFG_OPT_W3_WPS: return o.w3_wps;
+    case DFG_OPT_W3_RPC: return o.w3_rpc;
+    case DFG_OPT_W3_SMALL_WPS: return o.w3_small_wps;
+    case DFG_OPT_CR_MARGIN: return o.cr_margin;
+    default: return NAN;
+    }
 }
 
 int dfg_filter(const uint8_t *d_in, int32_t H, int32_t W, int64_t in_pitch, uint8_t *d_out,
@@ -317,18 +359,7 @@ int enqueue_bands(HostCache &c, const uint8_t *h_in, int H, int W, uint8_t *h_ou
     const int h = (prm->family == DFG_IDENTITY) ? 0 : prm->window / 2;
     const long long pitch = 3LL * W;
     const size_t px = (size_t)H * W;
-    // band boundaries: geometric taper q (band k ~ q^k; q = 1: equal bands)
-    // -- later bands smaller, so the kernel + D2H tail after the last copy
-    // is short
-    static const double taper = [] {
-        const char *t = getenv("DFG_HOST_TAPER");  // diagnostics override
-        return t ? atof(t) : 1.0;
-    }();
-    auto row0 = [&](int k) {
-        if (k >= nb) return H;
-        if (taper == 1.0 || taper <= 0.0) return (int)((long long)k * H / nb);
-        return (int)(H * (1.0 - pow(taper, k)) / (1.0 - pow(taper, nb)));
-    };
+    auto row0 = [&](int k) { return k >= nb ? H : (int)((long long)k * H / nb); };  // equal bands
     const int nks = nb < kKStreams ? nb : kKStreams;
     cudaError_t e = cudaEventRecord(c.ev_start, st);  // buffers are free once prior work on `st` is done
     if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_in, c.ev_start, 0);
@@ -377,12 +408,6 @@ bool is_pinned(const void *p)
     return a.type == cudaMemoryTypeHost;
 }
 
-int env_int(const char *name, int dflt)
-{
-    const char *s = getenv(name);
-    return s ? atoi(s) : dflt;
-}
-
 }  // namespace
 
 extern "C" {
@@ -426,43 +451,10 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
         c.dev = dev;
     }
     const bool pinned = is_pinned(h_in) && is_pinned(h_out);
-    // Opt-in (DFG_HOST_STREAM=1) for 3x3 with pinned buffers: zero-copy
-    // streaming -- one launch of the warp row-sweep kernel reads the input
-    // rows from and writes the output rows to the mapped host buffers
-    // itself, as aligned words.  Measured slower than the banded copies
-    // below (1024^2: 263 us vs 140 us; kernel-issued partial-line writes to
-    // host memory run at ~17 GB/s), so off by default.
-    const bool stream_on = env_int("DFG_HOST_STREAM", 0) != 0;  // read per call (tests switch it)
-    if (stream_on && pinned && prm->window == 3 && prm->family != DFG_IDENTITY) {
-        cudaPointerAttributes ai, ao;
-        if (cudaPointerGetAttributes(&ai, h_in) == cudaSuccess && cudaPointerGetAttributes(&ao, h_out) == cudaSuccess &&
-            ai.devicePointer && ao.devicePointer) {
-            // diagnostics: DFG_HOST_STREAM=2 streams the input only (output
-            // via device memory + one D2H copy), 3 the output only
-            const int mode = env_int("DFG_HOST_STREAM", 1);
-            const uint8_t *kin = (const uint8_t *)ai.devicePointer;
-            uint8_t *kout = (uint8_t *)ao.devicePointer;
-            cudaError_t e = cudaSuccess;
-            if (mode == 3) {
-                e = cudaMemcpyAsync(c.d_in, h_in, 3 * px, cudaMemcpyHostToDevice, st);
-                kin = c.d_in;
-            }
-            if (mode == 2) kout = c.d_out;
-            if (e != cudaSuccess) return cuda_fail(e, "H2D");
-            rc = run(kin, H, W, 0, H, 3LL * W, 0, kout, 0, H, 3LL * W, 0, 1, prm, c.ws,
-                     dfg_workspace_bytes((int64_t)px), stream, nullptr, 0, 1);
-            if (rc) return rc;
-            if (mode == 2) e = cudaMemcpyAsync(h_out, c.d_out, 3 * px, cudaMemcpyDeviceToHost, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-            if (e != cudaSuccess) return cuda_fail(e, "synchronize");
-            return DFG_OK;
-        }
-        cudaGetLastError();
-    }
     const int h = (prm->family == DFG_IDENTITY) ? 0 : prm->window / 2;
-    static const int nb_env = env_int("DFG_HOST_BANDS", 0);  // diagnostics only
-    static const bool graph_on = env_int("DFG_HOST_GRAPH", 1) != 0;
-    const bool use_graph = pinned && graph_on;
+    const dfg::Options &opt = dfg::options();
+    const int nb_env = opt.host_bands;
+    const bool use_graph = pinned && opt.host_graph != 0;
     // Eager issue costs ~25 us of API calls per band, so bands only pay off
     // above ~0.5 M pixels each; a replayed graph has no per-band host cost,
     // but every copy still costs the copy engine ~5 us: measured best at
@@ -472,7 +464,7 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
     if (nb > H / 64) nb = H / 64;
     nb = nb < 1 ? 1 : (nb > kMaxBands ? kMaxBands : nb);
     if (prm->border == DFG_REFLECT && H <= 4 * h) nb = 1;
-    static const int w3_rpc = env_int("DFG_HOST_W3_RPC", 8);  // diagnostics override
+    const int w3_rpc = opt.host_w3_rpc;
     cudaError_t e;
     if (use_graph) {
         GraphEntry *g = nullptr, *victim = &c.graphs[0];
@@ -565,15 +557,11 @@ struct FrameCache {
 };
 thread_local FrameCache g_frames;
 
-// slots in use (DFG_FRAME_SLOTS: diagnostics override, 1..8)
+// slots in use (DFG_OPT_FRAME_SLOTS, 1..8); fixed by the first allocation
 int frame_slots()
 {
-    static const int n = [] {
-        const char *e = getenv("DFG_FRAME_SLOTS");
-        const int v = e ? atoi(e) : 4;
-        return v < 1 ? 1 : (v > kFrameSlots ? kFrameSlots : v);
-    }();
-    return n;
+    const int v = dfg::options().frame_slots;
+    return v < 1 ? 1 : (v > kFrameSlots ? kFrameSlots : v);
 }
 
 }  // namespace
@@ -642,6 +630,97 @@ int dfg_filter_host_frames(const uint8_t *const *h_in, uint8_t *const *h_out, in
     }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(e, "frame stream synchronize");
+    return DFG_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Run f(lo, hi) over [0, n) split into `threads` contiguous ranges.
+template <typename F>
+void parallel_ranges(size_t n, int threads, F &&f)
+{
+    if (threads <= 1 || n < (1u << 18)) {
+        f((size_t)0, n);
+        return;
+    }
+    std::vector<std::thread> pool;
+    pool.reserve(threads - 1);
+    const size_t step = (n + threads - 1) / threads;
+    for (int t = 1; t < threads; t++) {
+        const size_t lo = (size_t)t * step, hi = lo + step < n ? lo + step : n;
+        if (lo < hi) pool.emplace_back([&f, lo, hi] { f(lo, hi); });
+    }
+    f((size_t)0, step < n ? step : n);
+    for (std::thread &t : pool) t.join();
+}
+
+// Pinned uint8 staging of the float64 host path (per thread, grows).
+struct F64Staging {
+    uint8_t *in = nullptr, *out = nullptr;
+    size_t cap = 0;
+    void release()
+    {
+        if (in) cudaFreeHost(in);
+        if (out) cudaFreeHost(out);
+        in = out = nullptr;
+        cap = 0;
+    }
+    ~F64Staging() { release(); }
+};
+thread_local F64Staging g_f64;
+
+}  // namespace
+
+extern "C" {
+
+int dfg_filter_host_f64(const double *h_in, int32_t H, int32_t W, double *h_out, const dfg_params *prm,
+                        int32_t threads, void *stream)
+{
+    int rc = validate(prm);
+    if (rc) return rc;
+    if (H < 1 || W < 1) return fail(DFG_E_ARG, "image must contain at least one pixel");
+    if (!h_in || !h_out) return fail(DFG_E_ARG, "null host pointer");
+    const size_t n = 3 * (size_t)H * W;
+    if (threads <= 0) {
+        const unsigned hc = std::thread::hardware_concurrency();
+        threads = hc ? (int)hc : 1;
+    }
+    if (threads > 256) threads = 256;
+    F64Staging &g = g_f64;
+    if (g.cap < n) {
+        g.release();
+        cudaError_t e = cudaHostAlloc((void **)&g.in, n, cudaHostAllocDefault);
+        if (e == cudaSuccess) e = cudaHostAlloc((void **)&g.out, n, cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+            g.release();
+            return cuda_fail(e, "pinned staging allocation");
+        }
+        g.cap = n;
+    }
+    // float64 -> uint8 with the GPU path's one input restriction: integral
+    // values in 0..255 (NaN and infinities fail the range test)
+    std::atomic<unsigned> bad{0};
+    uint8_t *st = g.in;
+    parallel_ranges(n, threads, [&](size_t lo, size_t hi) {
+        unsigned b = 0;
+        for (size_t i = lo; i < hi; i++) {
+            const double v = h_in[i];
+            const double c = (v >= 0.0 && v <= 255.0) ? v : -1.0;
+            const int iv = (int)c;
+            b |= (unsigned)((double)iv != c) | (unsigned)(iv < 0);
+            st[i] = (uint8_t)iv;
+        }
+        if (b) bad.store(1u, std::memory_order_relaxed);
+    });
+    if (bad.load()) return fail(DFG_E_ARG, "pixel values must be integers in 0..255 on the GPU path");
+    rc = dfg_filter_host(g.in, H, W, g.out, prm, stream);
+    if (rc) return rc;
+    const uint8_t *so = g.out;
+    parallel_ranges(n, threads, [&](size_t lo, size_t hi) {
+        for (size_t i = lo; i < hi; i++) h_out[i] = (double)so[i];
+    });
     return DFG_OK;
 }
 

@@ -64,6 +64,29 @@ __device__ __forceinline__ double next_double(u128 &s, const u128 inc)
 constexpr int kRun = 64;      // pairs per thread run
 constexpr int kThreads = 256;
 
+// fixed-order block reduction -> one partial triple per block
+__device__ void block_reduce3(double acc0, double acc1, double acc2, double *partials)
+{
+    __shared__ double red[3][kThreads];
+    red[0][threadIdx.x] = acc0;
+    red[1][threadIdx.x] = acc1;
+    red[2][threadIdx.x] = acc2;
+    __syncthreads();
+    for (int w = kThreads / 2; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + w];
+            red[1][threadIdx.x] += red[1][threadIdx.x + w];
+            red[2][threadIdx.x] += red[2][threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        partials[3 * blockIdx.x + 0] = red[0][0];
+        partials[3 * blockIdx.x + 1] = red[1][0];
+        partials[3 * blockIdx.x + 2] = red[2][0];
+    }
+}
+
 struct Sample {
     double b, a;
 };
@@ -124,28 +147,53 @@ __global__ void __launch_bounds__(kThreads) dfg_calib_kernel(dfg_calib_params cp
         }
     }
     if (mode == 3) return;
-    // fixed-order block reduction -> one partial triple per block
-    __shared__ double red[3][kThreads];
-    red[0][threadIdx.x] = acc0;
-    red[1][threadIdx.x] = acc1;
-    red[2][threadIdx.x] = acc2;
-    __syncthreads();
-    for (int w = kThreads / 2; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) {
-            red[0][threadIdx.x] += red[0][threadIdx.x + w];
-            red[1][threadIdx.x] += red[1][threadIdx.x + w];
-            red[2][threadIdx.x] += red[2][threadIdx.x + w];
+    block_reduce3(acc0, acc1, acc2, partials);
+}
+
+// The same three reductions over stored samples (reference fit_line,
+// calibration.py:47-80, on caller-provided (b, a) arrays).
+__global__ void __launch_bounds__(kThreads) dfg_array_reduce_kernel(const double *__restrict__ b,
+                                                                    const double *__restrict__ a, long long n,
+                                                                    int mode, double x0, double x1,
+                                                                    double *partials)
+{
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (long long i = blockIdx.x * (long long)kThreads + threadIdx.x; i < n; i += (long long)gridDim.x * kThreads) {
+        const double sb = b[i], sa = a[i];
+        if (mode == 0) {
+            acc0 += sb;
+            acc1 += sa;
+        } else if (mode == 1) {
+            const double db = sb - x0, da = sa - x1;
+            acc0 += db * db;
+            acc1 += da * da;
+            acc2 += db * da;
+        } else {
+            const double r = sa - (x0 * sb + x1);
+            acc0 += r * r;
+            acc1 += fabs(r);
         }
-        __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        partials[3 * blockIdx.x + 0] = red[0][0];
-        partials[3 * blockIdx.x + 1] = red[1][0];
-        partials[3 * blockIdx.x + 2] = red[2][0];
-    }
+    block_reduce3(acc0, acc1, acc2, partials);
 }
 
 constexpr int kBlocks = 148 * 8;
+
+// per-block partial triples -> out3, summed in block order on the host
+// (kBlocks x 3 doubles: a fixed-order, deterministic final reduction)
+int sum_partials(const double *part, double *out3, cudaStream_t st)
+{
+    static thread_local double host[kBlocks * 3];
+    if (cudaMemcpyAsync(host, part, sizeof host, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFG_E_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return DFG_E_CUDA;
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int b = 0; b < kBlocks; b++)
+        for (int k = 0; k < 3; k++) s[k] += host[3 * b + k];
+    out3[0] = s[0];
+    out3[1] = s[1];
+    out3[2] = s[2];
+    return DFG_OK;
+}
 
 }  // namespace
 
@@ -161,16 +209,21 @@ extern "C" DFG_API int dfg_calib_reduce(const dfg_calib_params *cp, int32_t mode
     double *part = (double *)d_scratch;
     dfg_calib_kernel<<<kBlocks, kThreads, 0, st>>>(*cp, mode, x0, x1, part, nullptr, nullptr);
     if (cudaGetLastError() != cudaSuccess) return DFG_E_CUDA;
-    static thread_local double host[kBlocks * 3];
-    if (cudaMemcpyAsync(host, part, sizeof host, cudaMemcpyDeviceToHost, st) != cudaSuccess) return DFG_E_CUDA;
-    if (cudaStreamSynchronize(st) != cudaSuccess) return DFG_E_CUDA;
-    double s[3] = {0.0, 0.0, 0.0};
-    for (int b = 0; b < kBlocks; b++)
-        for (int k = 0; k < 3; k++) s[k] += host[3 * b + k];
-    out3[0] = s[0];
-    out3[1] = s[1];
-    out3[2] = s[2];
-    return DFG_OK;
+    return sum_partials(part, out3, st);
+}
+
+extern "C" DFG_API int dfg_moments_reduce(const double *d_b, const double *d_a, int64_t n, int32_t mode, double x0,
+                                          double x1, double *out3, void *d_scratch, size_t scratch_bytes,
+                                          void *stream)
+{
+    if (!d_b || !d_a || !out3 || !d_scratch || n < 1 || mode < 0 || mode > 2 ||
+        scratch_bytes < dfg_calib_scratch_bytes())
+        return DFG_E_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    double *part = (double *)d_scratch;
+    dfg_array_reduce_kernel<<<kBlocks, kThreads, 0, st>>>(d_b, d_a, n, mode, x0, x1, part);
+    if (cudaGetLastError() != cudaSuccess) return DFG_E_CUDA;
+    return sum_partials(part, out3, st);
 }
 
 extern "C" DFG_API int dfg_calib_samples(const dfg_calib_params *cp, double *d_b, double *d_a, void *stream)

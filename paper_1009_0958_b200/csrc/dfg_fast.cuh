@@ -33,8 +33,6 @@
 // acosf(dot * rsqrt * rsqrt) loses ~1% of decisions.
 #pragma once
 
-#include <stdlib.h>
-
 #include <type_traits>
 
 #include "dfg_f64.cuh"
@@ -1243,16 +1241,15 @@ template <int S, int FAM, int ST, int PC>
 cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp)
 {
     if constexpr (S == 3) {
-        // 3x3: the warp-synchronous row-sweep kernel (dfg_w3.cuh); the CTA
-        // kernel stays selectable for comparison (DFG_S3_CTA=1)
-        // for very small inputs (< 8 K strip-rows, e.g. 256^2) the CTA
-        // kernel's finer tiles win; from C1's 512^2 (9 K strip-rows, 28 vs
-        // 35 us on the config image) the row sweep does
-        // (DFG_S3_KERNEL=cta|w3 forces one; read per call so tests can switch)
-        const char *force = getenv("DFG_S3_KERNEL");
+        // 3x3: the warp-synchronous row-sweep kernel (dfg_w3.cuh) from C1's
+        // 512^2 up (9 K strip-rows: 28 vs 35 us on the config image); for
+        // very small inputs (< 8 K strip-rows, e.g. 256^2) the CTA kernel's
+        // finer tiles win.  DFG_OPT_S3_SCHEDULE forces one (both are
+        // parity-tested).
+        const int force = options().s3_schedule;
         const long long strip_rows = (long long)((kp.W + 29) / 30) * kp.out_rows * kp.n_frames;
-        const bool w3 = kp.hostio || (kp.in_pitch <= 0xffffffffLL &&
-                                      (force ? (force[0] == 'w') : (kp.w3_rpc > 0 || strip_rows >= 8192)));
+        const bool w3 = kp.in_pitch <= 0xffffffffLL &&
+                        (force ? force == 1 : (kp.w3_rpc > 0 || strip_rows >= 8192));
         if (w3) return launch_w3<FAM, ST, PC>(st, in, out, kp);
     }
     using SH = Shape<S, FAM>;

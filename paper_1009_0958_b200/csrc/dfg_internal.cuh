@@ -62,18 +62,27 @@ struct KParams {
     // 3x3 schedule hint: > 0 = the warp row-sweep kernel with this many rows
     // per chunk (host pipeline bands: short latency, overlapping launches)
     int w3_rpc;
-    // 1: in / out are mapped pinned host buffers (3x3 zero-copy host path)
-    int hostio;
-    // diagnostics only (DFG_DIAG_NO_FIXUP=1): skip the float64 re-decision,
-    // to time its share -- results may then differ from the reference
+    // diagnostics only (DFG_OPT_NO_FIXUP): skip the float64 re-decision, to
+    // time its share -- results may then differ from the reference
     int diag_no_fixup;
-    // diagnostics only (DFG_DIAG_CYCLES=1): SM cycles spent in the float64
-    // re-decision, summed into the 64-bit counter at flag_count + 4
-    int diag_cycles;
-    // > 0: capacity (entries) of the 3x3 row sweep's deferred float64
-    // re-decision queue in the workspace (dfg_w3.cuh); 0: re-decide inline
-    int w3_queue;
 };
+
+// Process-wide schedule / diagnostic options (dfg_set_option, include/
+// dirfilt_gpu.h): read by the host launch code, never from the environment.
+struct Options {
+    int s3_schedule = 0;    // DFG_OPT_S3_SCHEDULE: 0 auto, 1 warp row sweep, 2 CTA tiles
+    int no_fixup = 0;       // DFG_OPT_NO_FIXUP (diagnostics: results may differ)
+    int host_bands = 0;     // DFG_OPT_HOST_BANDS: 0 auto
+    int host_graph = 1;     // DFG_OPT_HOST_GRAPH
+    int host_w3_rpc = 8;    // DFG_OPT_HOST_W3_RPC: rows per chunk of the host pipeline's 3x3 band kernels
+    int frame_slots = 4;    // DFG_OPT_FRAME_SLOTS: device slots of dfg_filter_host_frames (1..8)
+    int w3_wps = 0;         // DFG_OPT_W3_WPS: resident warps per SM the 3x3 chunking targets (0 auto)
+    int w3_rpc = 0;         // DFG_OPT_W3_RPC: rows per chunk of the 3x3 row sweep (0 auto)
+    int w3_small_wps = 12;  // DFG_OPT_W3_SMALL_WPS: warps per SM for single-wave 3x3 frames
+    double cr_margin = 1e-12;  // DFG_OPT_CR_MARGIN: relative margin that triggers the CR-acos pass
+};
+Options &options();
+int sm_count(int dev);  // multiProcessorCount, cached per device
 
 // Border policy resolution (image.py:158-176): replicate = clamp,
 // reflect = numpy 'symmetric' (edge-inclusive mirror, periodic).

@@ -39,8 +39,7 @@ struct W3Cfg {
     // du <= 1 entries of the previous row and du = 0 entries two rows up
     static constexpr int E_BYTES = (3 * 7 + 5) * 32 * (int)sizeof(DT);
     static constexpr int F64_BYTES = 9 * (int)sizeof(E64) + 2 * 36 * 8 + 16;
-    static constexpr int OUT_BYTES = 96;  // host-I/O output row staging (30 pixels)
-    static constexpr int WARP_BYTES = (REC_BYTES + COL_BYTES + E_BYTES + F64_BYTES + OUT_BYTES + 15) & ~15;
+    static constexpr int WARP_BYTES = (REC_BYTES + COL_BYTES + E_BYTES + F64_BYTES + 15) & ~15;
     static constexpr size_t kSmem = (size_t)WARPS * WARP_BYTES;
 };
 
@@ -54,12 +53,6 @@ __host__ __device__ constexpr int w3_k(int du, int dv) { return du == 0 ? dv - 1
 template <int ST>
 constexpr int w3_minb() { return 8; }
 
-// HIO (host I/O): `in` / `out` are mapped pinned HOST buffers -- the kernel
-// streams its rows over PCIe itself (the host path's zero-copy mode): each
-// warp row is read as aligned 32-bit words (<= 25 per 32-pixel strip row,
-// bytes redistributed by shuffles) and written as aligned words assembled in
-// shared memory, so PCIe sees full coalesced requests in both directions
-// (full duplex) while the SMs compute.
 // Float64 re-decision of one window (whole warp): lane i < 9 holds the
 // packed colour of window pixel i; returns the chosen window index.
 template <int FAM, int ST>
@@ -91,15 +84,14 @@ __device__ __forceinline__ int w3_decide64(const KParams &kp, unsigned char *f64
 }
 
 // Inline re-decision of the doubtful pixels `mask` of one output row segment
-// from the warp's ring (window row u of the output in ring slot sl[u]): the
-// host-I/O kernel, the host pipeline's band kernels and queue overflow.
+// from the warp's ring (window row u of the output in ring slot sl[u]), right
+// after the row step that found them.
 template <int FAM, int ST>
 __device__ __forceinline__ void w3_redecide(const KParams &kp, const uint32_t *rK, int sl0, int sl1, int sl2,
                                          unsigned char *f64b, unsigned mask, uint8_t *orow_px)
 {
     const int lane = threadIdx.x & 31;
     if (lane == 0) atomicAdd(kp.flag_count, (unsigned)__popc(mask));
-    const long long t0 = kp.diag_cycles ? clock64() : 0;
     while (mask) {
         const int fl = __ffs(mask) - 1;
         mask &= mask - 1;
@@ -112,119 +104,6 @@ __device__ __forceinline__ void w3_redecide(const KParams &kp, const uint32_t *r
             op[0] = (uint8_t)(kb & 0xff);
             op[1] = (uint8_t)((kb >> 8) & 0xff);
             op[2] = (uint8_t)((kb >> 16) & 0xff);
-        }
-    }
-    if (kp.diag_cycles && lane == 0)
-        atomicAdd(reinterpret_cast<unsigned long long *>(kp.flag_count + 4), (unsigned long long)(clock64() - t0));
-}
-
-// Deferred re-decision queue (kp.w3_queue): the sweep appends its doubtful
-// pixels {frame, out row, column, state} to the workspace instead of
-// stalling its row sweep for the float64 work, and every warp drains the
-// queue after its sweep, so the re-decisions spread over the warps that
-// finish first instead of lengthening the sweeps of the warps that found
-// them (the single-wave grid ends with its slowest warp).
-//
-// Workspace words after the diagnostic counters: [8] entries appended,
-// [9] tickets drawn, [10] CTAs done.  Entry state: 0 empty, 1 published,
-// 2 abandoned.  A drainer draws ticket t only when the queue looked
-// non-empty, then resolves entry t with one compare-and-swap: published ->
-// it re-decides the pixel; still empty (it raced past the producers) -> it
-// marks the entry abandoned and stops, and the producer that later appends
-// at t finds the mark and re-decides that pixel itself.  No warp ever
-// waits on another, every entry is re-decided exactly once, and the last
-// CTA resets the counters and the abandoned marks for the next call.
-constexpr int kQueueWord = 8;
-constexpr int kQueueEntryOffset = 256;  // bytes: entries follow the counter header
-
-__device__ __forceinline__ uint4 *w3_queue_entries(const KParams &kp)
-{
-    return reinterpret_cast<uint4 *>(reinterpret_cast<unsigned char *>(kp.flag_count) + kQueueEntryOffset);
-}
-
-// Re-decide the pixel of one published entry (whole warp), reading its
-// window from the input image.
-template <int FAM, int ST>
-__device__ __forceinline__ void w3_redecide_entry(const KParams &kp, const uint8_t *in, uint8_t *out,
-                                               unsigned char *f64b, uint4 en)
-{
-    const int lane = threadIdx.x & 31;
-    const int frame = (int)en.x, oy = (int)en.y, col = (int)en.z;
-    // window pixel i = lane: input row of output row oy - 1 + i / 3, column col - 1 + i % 3
-    uint32_t cc = 0u;
-    if (lane < 9) {
-        int gy = kp.out_row0 + oy - 1 + lane / 3;
-        if ((unsigned)gy >= (unsigned)kp.global_H) gy = resolve_idx(gy, kp.global_H, kp.border);
-        const int ry = min(max(gy - kp.in_row0, 0), kp.in_rows - 1);
-        const int cx = resolve_idx(col - 1 + lane % 3, kp.W, kp.border);
-        const uint8_t *px = in + (long long)frame * kp.in_fstride + (long long)ry * kp.in_pitch + 3 * cx;
-        cc = (uint32_t)px[0] | ((uint32_t)px[1] << 8) | ((uint32_t)px[2] << 16);
-    }
-    const int bb = w3_decide64<FAM, ST>(kp, f64b, cc);
-    const uint32_t kb = __shfl_sync(0xffffffffu, cc, bb);
-    if (lane == 0) {
-        uint8_t *op = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch + 3 * col;
-        op[0] = (uint8_t)(kb & 0xff);
-        op[1] = (uint8_t)((kb >> 8) & 0xff);
-        op[2] = (uint8_t)((kb >> 16) & 0xff);
-    }
-}
-
-// Drain the queue (whole warp), then retire the warp (its CTA's last warp
-// counts the CTA done; the grid's last CTA resets the queue).
-template <int FAM, int ST>
-__device__ __forceinline__ void w3_drain(const KParams &kp, const uint8_t *in, uint8_t *out, unsigned char *f64b,
-                                      unsigned cta_warps, unsigned total_ctas, unsigned *s_done)
-{
-    const int lane = threadIdx.x & 31;
-    unsigned *qc = kp.flag_count + kQueueWord;
-    uint4 *qe = w3_queue_entries(kp);
-    const unsigned cap = (unsigned)kp.w3_queue;
-    const long long t0 = kp.diag_cycles ? clock64() : 0;
-    bool any = false;
-    for (;;) {
-        // lane 0: 0 = stop, 1 = entry t to re-decide
-        unsigned t = 0, go = 0;
-        uint4 en = make_uint4(0, 0, 0, 0);
-        if (lane == 0) {
-            const unsigned pr = *reinterpret_cast<volatile unsigned *>(qc);
-            const unsigned tk = *reinterpret_cast<volatile unsigned *>(qc + 1);
-            if (tk < min(pr, cap)) {
-                t = atomicAdd(qc + 1, 1u);
-                if (t < cap) {
-                    const unsigned old = atomicCAS(&qe[t].w, 0u, 2u);  // empty -> abandoned
-                    if (old == 1u) {                                   // published
-                        __threadfence();
-                        const volatile uint4 *ve = qe + t;
-                        en = make_uint4(ve->x, ve->y, ve->z, 0u);
-                        qe[t].w = 0u;  // consumed: clean for the next call
-                        go = 1;
-                    }
-                }
-            }
-        }
-        go = __shfl_sync(0xffffffffu, go, 0);
-        if (!go) break;
-        any = true;
-        en.x = __shfl_sync(0xffffffffu, en.x, 0);
-        en.y = __shfl_sync(0xffffffffu, en.y, 0);
-        en.z = __shfl_sync(0xffffffffu, en.z, 0);
-        w3_redecide_entry<FAM, ST>(kp, in, out, f64b, en);
-    }
-    if (lane == 0) {
-        if (kp.diag_cycles && any)
-            atomicAdd(reinterpret_cast<unsigned long long *>(kp.flag_count + 4), (unsigned long long)(clock64() - t0));
-        if (atomicAdd(s_done, 1u) == cta_warps - 1) {  // this CTA's last warp
-            __threadfence();
-            if (atomicAdd(qc + 2, 1u) == total_ctas - 1) {  // the grid's last CTA: reset
-                const unsigned pr = min(*reinterpret_cast<volatile unsigned *>(qc), cap);
-                const unsigned tk = min(*reinterpret_cast<volatile unsigned *>(qc + 1), cap);
-                for (unsigned i = pr; i < tk; i++) qe[i].w = 0u;  // tickets drawn past the last entry
-                qc[0] = 0u;
-                qc[1] = 0u;
-                qc[2] = 0u;
-                __threadfence();
-            }
         }
     }
 }
@@ -242,7 +121,7 @@ __device__ __forceinline__ void w3_drain(const KParams &kp, const uint8_t *in, u
 // The values are the ring entries of the 36 window pairs' lower pixels, each
 // loaded by the lane of P_t (the sums cover every other window pixel once,
 // so the error budget's (n-1)-term summation bound holds unchanged).
-template <int FAM, int ST, int PC, bool HIO, int MINB>
+template <int FAM, int ST, int PC, int MINB>
 __global__ void __launch_bounds__(64, MINB)
 dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const __grid_constant__ KParams kp, int n_strips,
               int n_chunks)
@@ -254,10 +133,7 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
     constexpr int N = 9, DC = 4;
 
     extern __shared__ __align__(16) unsigned char w3_smem[];
-    __shared__ unsigned s_done;  // warps of this CTA done draining
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_done = 0;
-    __syncthreads();
     const int gw = blockIdx.x * C::WARPS + warp;  // global warp id within the frame
     if (gw >= n_strips * n_chunks) return;        // whole warp exits together
     const int strip = gw % n_strips, chunk = gw / n_strips;
@@ -271,7 +147,6 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
     DT *rE = reinterpret_cast<DT *>(wb + C::REC_BYTES + C::COL_BYTES);  // [3][7][32] + [5][32]
     DT *rE2 = rE + 3 * 7 * 32;
     unsigned char *f64b = wb + C::REC_BYTES + C::COL_BYTES + C::E_BYTES;
-    uint8_t *ostage = f64b + C::F64_BYTES;  // HIO output row staging
 
     const int col = strip * 30 - 1 + lane;  // input column of this lane
     const int colr = resolve_idx(col, kp.W, kp.border);
@@ -308,42 +183,8 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
         g = npx[1];
         b = npx[2];
     };
-    // HIO: in-range columns [c_lo, c_hi) of this strip arrive as the aligned
-    // words covering their bytes (an aligned word never crosses a page, so
-    // the over-read at either end is harmless); out-of-range (border) lanes
-    // load their resolved column's bytes directly
-    const int c_lo = max(strip * 30 - 1, 0), c_hi = min(strip * 30 + 31, kp.W);
-    const bool in_range = col >= 0 && col < kp.W;
-    struct Pend {
-        uint32_t word, r, g, b;
-        int mis;  // byte offset of column c_lo within its aligned word
-    };
-    auto load_hio = [&](int yy, Pend &pd) {
-        const uint8_t *rowp = fin + (size_t)((unsigned long long)(unsigned)row_of(yy) * pitch);
-        const uintptr_t lo = (uintptr_t)(rowp + 3 * c_lo), hi = (uintptr_t)(rowp + 3 * c_hi);
-        const uintptr_t wa = (lo & ~(uintptr_t)3) + 4 * (uintptr_t)lane;
-        pd.mis = (int)(lo & 3);
-        pd.word = wa < hi ? *reinterpret_cast<const uint32_t *>(wa) : 0u;
-        if (!in_range) {
-            const uint8_t *px = rowp + colr * 3;
-            pd.r = px[0];
-            pd.g = px[1];
-            pd.b = px[2];
-        }
-    };
-    auto unpack_hio = [&](const Pend &pd, uint32_t &r, uint32_t &g, uint32_t &b) {
-        const int off = 3 * (max(col, 0) - c_lo) + pd.mis;
-        const uint32_t w0 = __shfl_sync(0xffffffffu, pd.word, (off >> 2) & 31);
-        const uint32_t w1 = __shfl_sync(0xffffffffu, pd.word, ((off >> 2) + 1) & 31);
-        const uint32_t v = __funnelshift_r(w0, w1, 8 * (off & 3));
-        r = in_range ? (v & 0xffu) : pd.r;
-        g = in_range ? ((v >> 8) & 0xffu) : pd.g;
-        b = in_range ? ((v >> 16) & 0xffu) : pd.b;
-    };
     uint32_t nr8 = 0, ng8 = 0, nb8 = 0;
-    Pend pend{};
-    if constexpr (HIO) load_hio(oy0 - 1, pend);
-    else load_px(oy0 - 1, nr8, ng8, nb8);
+    load_px(oy0 - 1, nr8, ng8, nb8);
     // this lane's pixels of the previous two row steps (the vertical pair's
     // partners for lane l-2); neutral until the warm-up steps fill them
     Pix pm1 = {1.f, 1.f, 1.f, 1.f}, pm2 = {1.f, 1.f, 1.f, 1.f};
@@ -352,16 +193,8 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
     auto step = [&](const int S0, const int S1, const int S2, const int y) -> unsigned {
         __syncwarp();  // the previous step's readers are done with this slot
         // ---- 1. stage the new pixel ---------------------------------------
-        uint32_t r8, g8, b8;
-        if constexpr (HIO) {
-            unpack_hio(pend, r8, g8, b8);
-            if (y < oy1) load_hio(y + 1, pend);
-        } else {
-            r8 = nr8;
-            g8 = ng8;
-            b8 = nb8;
-            if (y < oy1) load_px(y + 1, nr8, ng8, nb8);
-        }
+        const uint32_t r8 = nr8, g8 = ng8, b8 = nb8;
+        if (y < oy1) load_px(y + 1, nr8, ng8, nb8);
         const uint32_t rgb = r8 | (g8 << 8) | (b8 << 16);
         const bool zero = rgb == 0u;
         // gray map: the zero vector -> (1, 1, 1) (its channels are 0, so OR-ing
@@ -569,66 +402,14 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
                 }
             }
         }
-        // ---- 4. doubtful pixels: queued for the drain, or re-decided inline
-        // by the caller (one call site) ----------------------------------------
-        unsigned mask = __ballot_sync(0xffffffffu, valid && doubt && !kp.diag_no_fixup);
-        bool queued = false;
-        if (!HIO && mask && kp.w3_queue) {
-            unsigned base = 0;
-            if (lane == 0) {
-                base = atomicAdd(kp.flag_count + kQueueWord, (unsigned)__popc(mask));
-                atomicAdd(kp.flag_count, (unsigned)__popc(mask));
-            }
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if ((mask >> lane) & 1u) {
-                const unsigned idx = base + __popc(mask & ((1u << lane) - 1u));
-                if (idx < (unsigned)kp.w3_queue) {
-                    uint4 *qe = w3_queue_entries(kp) + idx;
-                    qe->x = (unsigned)frame;
-                    qe->y = (unsigned)oy;
-                    qe->z = (unsigned)col;
-                    __threadfence();
-                    // publish; a drainer that raced ahead left it abandoned
-                    // (2): then this lane's pixel is re-decided inline
-                    if (atomicCAS(&qe->w, 0u, 1u) == 0u) queued = true;
-                    else qe->w = 0u;
-                }
-            }
-            mask &= ~__ballot_sync(0xffffffffu, queued);  // queue overflow: re-decided inline
-            if (mask && lane == 0) atomicAdd(kp.flag_count, 0u - (unsigned)__popc(mask));  // counted inline
-        }
-        if (valid && !queued) {
-            uint8_t *op = HIO ? ostage + 3 * (lane - 1) : orow + col * 3;
+        // ---- 4. write; doubtful pixels are re-decided by the caller ---------
+        if (valid) {
+            uint8_t *op = orow + col * 3;
             op[0] = (uint8_t)(cb & 0xff);
             op[1] = (uint8_t)((cb >> 8) & 0xff);
             op[2] = (uint8_t)((cb >> 16) & 0xff);
         }
-        if constexpr (HIO) {
-            if (mask) w3_redecide<FAM, ST>(kp, rK, S0, S1, S2, f64b, mask, ostage);
-            // the staged row segment -> host as aligned words
-            __syncwarp();
-            const int nv = min(30, kp.W - strip * 30);
-            if (oy < oy1 && nv > 0) {
-                const uintptr_t A = (uintptr_t)(orow + 3 * (strip * 30)), E = A + 3 * (uintptr_t)nv;
-                const uintptr_t wa = (A & ~(uintptr_t)3) + 4 * (uintptr_t)lane;
-                if (wa < E) {
-                    if (wa >= A && wa + 4 <= E) {
-                        const int o = (int)(wa - A);
-                        *reinterpret_cast<uint32_t *>(wa) = (uint32_t)ostage[o] | ((uint32_t)ostage[o + 1] << 8) |
-                                                            ((uint32_t)ostage[o + 2] << 16) |
-                                                            ((uint32_t)ostage[o + 3] << 24);
-                    } else {
-                        for (int k = 0; k < 4; k++) {
-                            const uintptr_t a = wa + k;
-                            if (a >= A && a < E) *reinterpret_cast<uint8_t *>(a) = ostage[a - A];
-                        }
-                    }
-                }
-            }
-            return 0u;
-        } else {
-            return mask;
-        }
+        return __ballot_sync(0xffffffffu, valid && doubt && !kp.diag_no_fixup);
     };
     int s0 = 0, s1 = 2, s2 = 1;  // ring slots of rows y, y-1, y-2 (rotated each step)
     for (int y = oy0 - 1; y <= oy1; y++) {
@@ -642,11 +423,6 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
         s1 = s0;
         s0 = t;
     }
-    if (!HIO && kp.w3_queue) {
-        const int per_frame = n_strips * n_chunks;
-        const unsigned cta_warps = (unsigned)min(C::WARPS, per_frame - (int)blockIdx.x * C::WARPS);
-        w3_drain<FAM, ST>(kp, in, out, f64b, cta_warps, gridDim.x * gridDim.z, &s_done);
-    }
 }
 
 template <int FAM, int ST, int PC>
@@ -654,42 +430,32 @@ cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KP
 {
     using C = W3Cfg<FAM>;
     constexpr int minb = w3_minb<ST>();
-    auto kern = kp.hostio ? dfg_w3_kernel<FAM, ST, PC, true, minb> : dfg_w3_kernel<FAM, ST, PC, false, minb>;
-    static unsigned long long configured[2] = {};
+    auto kern = dfg_w3_kernel<FAM, ST, PC, minb>;
+    static unsigned long long configured = 0;
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!(configured[kp.hostio] & (1ull << (dev & 63)))) {
+    if (!(configured & (1ull << (dev & 63)))) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
         if (e != cudaSuccess) return e;
-        configured[kp.hostio] |= 1ull << (dev & 63);
+        configured |= 1ull << (dev & 63);
     }
+    const Options &opt = options();
+    const long long sms = sm_count(dev);
     const int n_strips = (kp.W + 29) / 30;
-    // chunks per strip: fill whole waves of resident warps (WPS per SM) with
+    // chunks per strip: fill whole waves of resident warps (wps per SM) with
     // equal row counts (chunk c covers rows [c R / n, (c+1) R / n)), at most
     // 64 rows per chunk; every chunk pays 2 warm-up row steps
-    static const int env_wps = [] {
-        const char *e = getenv("DFG_W3_WPS");  // diagnostics only
-        return e ? atoi(e) : 0;
-    }();
-    static const int rpc_env = [] {
-        const char *e = getenv("DFG_W3_RPC");  // diagnostics only
-        return e ? atoi(e) : 0;
-    }();
     const long long cols = (long long)n_strips * kp.n_frames;  // independent strip columns
     const long long strip_rows = cols * kp.out_rows;
     // small single-wave frames (< 8 rows per chunk at 16 warps per SM): 12
     // warps per SM with longer chunks (C1 512^2: 22.6 -> 21.0 us; C2's 15-row
     // chunks stay at 16 warps: 12 measured 4.5 % slower there)
-    static const int small_wps = [] {
-        const char *e = getenv("DFG_W3_SMALL_WPS");  // diagnostics only
-        return e ? atoi(e) : 12;
-    }();
-    long long wps = env_wps > 0 ? env_wps : 2 * minb;
-    if (env_wps <= 0 && small_wps > 0 && strip_rows < 8LL * 148 * wps) wps = small_wps;
-    const long long slots = 148 * wps;
+    long long wps = opt.w3_wps > 0 ? opt.w3_wps : 2 * minb;
+    if (opt.w3_wps <= 0 && opt.w3_small_wps > 0 && strip_rows < 8LL * sms * wps) wps = opt.w3_small_wps;
+    const long long slots = sms * wps;
     const long long waves = (strip_rows + slots * 64 - 1) / (slots * 64);
     long long n_chunks = (waves * slots) / cols;
-    const int rpc_hint = rpc_env > 0 ? rpc_env : kp.w3_rpc;  // host pipeline bands: short chunks
+    const int rpc_hint = opt.w3_rpc > 0 ? opt.w3_rpc : kp.w3_rpc;  // host pipeline bands: short chunks
     if (rpc_hint > 0) n_chunks = (kp.out_rows + rpc_hint - 1) / rpc_hint;
     n_chunks = n_chunks < 1 ? 1 : (n_chunks > kp.out_rows ? kp.out_rows : n_chunks);
     n_chunks = n_chunks < (kp.out_rows + 63) / 64 ? (kp.out_rows + 63) / 64 : n_chunks;

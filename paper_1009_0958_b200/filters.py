@@ -25,7 +25,7 @@ import threading
 import numpy as np
 
 from . import _lib
-from .image import REPLICATE, RasterImage, to_uint8
+from .image import REPLICATE, RasterImage
 
 _ws_lock = threading.Lock()
 _ws_cache: dict = {}
@@ -106,18 +106,18 @@ def _validate_spec(spec) -> None:
 
 
 def workspace(nbytes: int, device=None, stream=None):
-    """A cached, zeroed device workspace of at least ``nbytes`` for
-    ``device``, one per stream: a workspace serves one call at a time (it
-    holds the row sweep's re-decision queue), and calls on one stream are
-    ordered."""
+    """A cached, zeroed device workspace (the diagnostic counters) of at least
+    ``nbytes`` for ``device``.  Calls only add to its counters, so every
+    stream of a device shares one; it is allocated and zeroed synchronously,
+    so it is ready before any stream's first launch."""
     torch = _torch()
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
-    key = (dev.index, _stream_ptr(torch, stream, dev).value)
     with _ws_lock:
-        buf = _ws_cache.get(key)
+        buf = _ws_cache.get(dev.index)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.zeros(max(nbytes, 1 << 20), dtype=torch.uint8, device=dev)
-            _ws_cache[key] = buf
+            buf = torch.zeros(max(nbytes, 4096), dtype=torch.uint8, device=dev)
+            torch.cuda.synchronize(dev)  # zero-fill done before launches on any stream
+            _ws_cache[dev.index] = buf  # (a replaced buffer only ever held counters)
         return buf
 
 
@@ -126,6 +126,16 @@ def _stream_ptr(torch, stream, device):
         return ctypes.c_void_p(stream.cuda_stream)
     idx = torch.cuda.current_device() if device is None else torch.device(device).index
     return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(idx))  # no Stream object per call
+
+
+def _check_out(torch, out, shape, x):
+    """Caller-supplied output buffers: uint8 rows of packed pixels on x's device."""
+    if (not isinstance(out, torch.Tensor) or out.dtype != torch.uint8 or out.device != x.device or
+            tuple(out.shape) != tuple(shape) or out.stride(-1) != 1 or out.stride(-2) != 3):
+        raise ValueError(f"out must be a uint8 tensor of shape {tuple(shape)} on {x.device} with packed pixels "
+                         "(stride 3 between pixels, 1 between channels)")
+    if len(shape) == 4 and out.stride(1) * shape[1] > out.stride(0):
+        raise ValueError("out frames overlap (frame stride smaller than its rows)")
 
 
 def filter_device(x, spec, policy=REPLICATE, out=None, stream=None, ws=None):
@@ -139,6 +149,8 @@ def filter_device(x, spec, policy=REPLICATE, out=None, stream=None, ws=None):
     H, W = int(x.shape[0]), int(x.shape[1])
     if out is None:
         out = torch.empty((H, W, 3), dtype=torch.uint8, device=x.device)
+    else:
+        _check_out(torch, out, (H, W, 3), x)
     prm = _params(spec, policy)
     need = _lib.lib().dfg_workspace_bytes(H * W)
     if ws is None:
@@ -162,6 +174,8 @@ def filter_batch_device(x, spec, policy=REPLICATE, out=None, stream=None, ws=Non
     B, H, W = (int(s) for s in x.shape[:3])
     if out is None:
         out = torch.empty_like(x)
+    else:
+        _check_out(torch, out, (B, H, W, 3), x)
     prm = _params(spec, policy)
     need = _lib.lib().dfg_workspace_bytes(B * H * W)
     if ws is None:
@@ -183,10 +197,15 @@ def filter_rows_device(x, global_H, in_row0, out_row0, out_rows, spec, policy=RE
     ``_engine.py:560-583``)."""
     torch = _torch()
     _validate_spec(spec)
-    x = x.contiguous()
+    if x.dtype != torch.uint8 or x.dim() != 3 or x.shape[2] != 3 or not x.is_cuda:
+        raise ValueError("expected a CUDA uint8 tensor of shape (rows, W, 3)")
+    if x.stride(2) != 1 or x.stride(1) != 3:
+        x = x.contiguous()
     in_rows, W = int(x.shape[0]), int(x.shape[1])
     if out is None:
         out = torch.empty((out_rows, W, 3), dtype=torch.uint8, device=x.device)
+    else:
+        _check_out(torch, out, (out_rows, W, 3), x)
     prm = _params(spec, policy)
     need = _lib.lib().dfg_workspace_bytes(out_rows * W)
     if ws is None:
@@ -279,30 +298,35 @@ def last_fixup_count(device=None, stream=None) -> int:
 
 def apply_filter(img, spec, policy=REPLICATE, workers: int = 1, *, device=None) -> RasterImage:
     """Filter the whole image; output pixel (r, c) is the filter of the window
-    centred there, read from the original image.
+    centred there, read from the original image (reference
+    ``filters.apply_filter``, filters.py:379-433).
 
-    Same signature and semantics as the reference.  ``workers > 1``
-    partitions the output rows into that many bands, each filtered by its own
-    ``dfg_filter_rows`` call (the reference's row-threaded path); results are
-    bit-identical to ``workers=1``.  ``device`` (keyword-only addition)
-    selects the CUDA device.
+    Same signature, semantics and errors as the reference, plus one input
+    restriction of the GPU path: pixel values must be integers in 0..255
+    (``ValueError`` otherwise).  The float64 pixels go through the C ABI's
+    ``dfg_filter_host_f64`` (validation and conversion on the host cores,
+    pinned staging, banded H2D / kernels / D2H, float64 result); the
+    result is a new ``RasterImage``.  ``workers`` keeps the reference's
+    meaning (a row partition with bit-identical results): on the GPU the
+    rows are banded inside the call, so the value only needs to be accepted.
+    ``device`` (keyword-only addition) selects the CUDA device.
     """
     pixels = img.pixels if hasattr(img, "pixels") else np.asarray(img)
     if spec.family == "identity":  # filters.py:394-395
         return RasterImage._adopt(np.array(pixels, dtype=np.float64, copy=True))
     _validate_spec(spec)
-    u8 = to_uint8(pixels)
+    prm = _params(spec, policy)
+    a = pixels if (type(pixels) is np.ndarray and pixels.dtype == np.float64 and pixels.flags.c_contiguous) \
+        else np.ascontiguousarray(pixels, dtype=np.float64)
+    if a.ndim != 3 or a.shape[2] != 3:
+        raise ValueError(f"pixel array must have shape (M, N, 3), got {a.shape}")
     torch = _torch()
-    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index)
-    M, N = u8.shape[:2]
-    x = torch.from_numpy(u8).to(dev)
-    if workers > 1 and M > 1:
-        out = torch.empty_like(x)
-        bounds = np.linspace(0, M, min(workers, M) + 1).astype(int)
-        for r0, r1 in zip(bounds[:-1], bounds[1:]):
-            if r1 > r0:
-                filter_rows_device(x, M, 0, int(r0), int(r1 - r0), spec, policy, out=out[r0:r1])
-    else:
-        out = filter_device(x, spec, policy)
-    res = out.cpu().numpy()
-    return RasterImage._adopt(res.astype(np.float64))
+    M, N = a.shape[:2]
+    out = np.empty((M, N, 3), dtype=np.float64)
+    idx = torch.cuda.current_device() if device is None else torch.device(device).index
+    with _on_device(torch, torch.device("cuda", idx)):
+        rc = _lib.lib().dfg_filter_host_f64(a.ctypes.data_as(ctypes.c_void_p), M, N,
+                                            out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(prm), 0,
+                                            _stream_ptr(torch, None, torch.device("cuda", idx)))
+    _lib.check(rc)
+    return RasterImage._adopt(out)

@@ -1,16 +1,28 @@
-"""CPU: bench.py's multi-GPU work split -- C5a row strips with their halo
-rows (strong scaling) and the C5b frame split -- partitions the work exactly
-once per pixel at 1/2/4/8 ranks, and strips filtered independently (oracle,
-global border policy) reproduce the whole-frame result bit for bit.  Config
-shapes are shrunk so the check runs in seconds; the split logic is the one
-the GPU bench uses."""
+"""CPU: bench.py's work split and its command-line contract.
+
+* C5a at N > 1 is row-strip sharded through parallel.StripJob (the halo
+  exchange + chunked gather that tests/test_parallel.py runs multi-rank
+  with gloo); here: the workload kinds, scaling and pixel totals at 1/2/4/8
+  ranks, and that the strips StripJob cuts partition the frame.
+* C5b frames are split across ranks exactly once, each with its seed.
+* Both arms print the same ``config`` dict.
+* ``--gpus N`` outside torchrun re-launches the script under
+  torch.distributed.run with N ranks (exercised with the CPU reference arm:
+  rank 0 prints exactly one JSON line with n_gpus = N)."""
+
+import json
+import subprocess
+import sys
+from pathlib import Path
 
 import numpy as np
 import pytest
 
 import bench
-import oracle
-from paper_1009_0958_b200 import parse_filter_spec, synth
+from paper_1009_0958_b200 import synth
+from paper_1009_0958_b200.parallel import strip_rows
+
+ROOT = Path(__file__).resolve().parent.parent
 
 
 @pytest.fixture
@@ -26,31 +38,22 @@ def small_configs(monkeypatch):
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-def test_c5a_strips_partition_and_match(small_configs, world):
+def test_c5a_strips(small_configs, world):
     cfgs, img = small_configs
-    spec = parse_filter_spec(cfgs["c5a"]["spec"])
-    H = img.shape[0]
-    want = oracle.filter_image(img, spec, threads=1)
+    H, W = img.shape[:2]
     covered = np.zeros(H, int)
-    total = 0
     for rank in range(world):
         wl = bench.workload("c5a", rank, world)
+        assert wl["total_px"] == H * W
         if world == 1:
-            assert wl["kind"] == "image" and wl["x"] is img
+            assert wl["kind"] == "image" and wl["x"] is img and wl["scaling"] == "weak"
             covered += 1
-            total += wl["px"]
             continue
-        r0, n, i0 = wl["out_row0"], wl["out_rows"], wl["in_row0"]
-        assert wl["kind"] == "rows" and wl["scaling"] == "strong" and wl["total_px"] == img.shape[0] * img.shape[1]
-        assert (wl["x"] == img[i0:i0 + wl["x"].shape[0]]).all()
-        assert i0 == max(0, r0 - 3) and i0 + wl["x"].shape[0] == min(H, r0 + n + 3)  # 7x7: 3-row halo
-        covered[r0:r0 + n] += 1
-        total += wl["px"]
-        full = np.zeros_like(img)
-        full[i0:i0 + wl["x"].shape[0]] = wl["x"]  # global row index, only the strip + halo present
-        got = oracle.filter_image(full, spec, threads=1, rows=(r0, r0 + n))[r0:r0 + n]
-        assert (got == want[r0:r0 + n]).all(), (world, rank)
-    assert (covered == 1).all() and total == img.shape[0] * img.shape[1]
+        assert wl["kind"] == "strips" and wl["scaling"] == "strong" and wl["x"] is img
+        r0, r1, i0, i1 = strip_rows(H, world, rank, 7)
+        assert i0 == max(0, r0 - 3) and i1 == min(H, r1 + 3)  # 7x7: 3-row halo
+        covered[r0:r1] += 1
+    assert (covered == 1).all()
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
@@ -67,3 +70,22 @@ def test_c5b_frame_split(small_configs, world):
             assert (fr == synth.noisy_image(12, 17, c["seed"] + f, c["noise"])).all()
             seen.append(f)
     assert sorted(seen) == list(range(c["frames"]))
+
+
+def test_default_workload_is_c5a():
+    assert bench.DEFAULT_CONFIG == "c5a"
+    d = bench.config_dict("c5a", 1)
+    assert d["workload"] == "c5a" and d["shape"] == [8192, 8192] and d["spec"] == "ddf:exact:window=7"
+
+
+def test_gpus_flag_relaunches_under_torchrun():
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--impl", "reference",
+                        "--config", "c1", "--steps", "1", "--warmup", "3"],
+                       capture_output=True, text=True, timeout=600, cwd=str(ROOT))
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["config"] == bench.config_dict("c1", 2)
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] in ("reference", "port")

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
+from paper_1009_0958_b200 import _lib
 from paper_1009_0958_b200 import (
     REFLECT, REPLICATE, CenterWeightedSpec, RasterImage, apply_filter, filter_device, parse_filter_spec, synth,
 )
@@ -39,11 +40,14 @@ CW = [("cwvmf", 2, "exact", 2.0, 3), ("cwvmf", 4, "exact", 1.0, 3), ("cwddf", 2,
 
 @pytest.mark.parametrize("kernel", ["w3", "cta"])
 @pytest.mark.parametrize("fam,k,strat,p,win", CW)
-def test_against_oracle(cuda, fam, k, strat, p, win, kernel, monkeypatch):
-    torch = cuda
+def test_against_oracle(cuda, fam, k, strat, p, win, kernel):
     if win != 3 and kernel == "cta":
         pytest.skip("one schedule for 5x5/7x7")
-    monkeypatch.setenv("DFG_S3_KERNEL", kernel)
+    with _lib.option("s3_schedule", 1 if kernel == "w3" else 2):
+        _check(cuda, fam, k, strat, p, win)
+
+
+def _check(torch, fam, k, strat, p, win):
     s = _spec({"family": fam, "k": k, "strategy": strat, "p": p, "window": win})
     for H, W, seed, border in ((97, 61, 3, "replicate"), (40, 29, 4, "reflect")):
         img = synth.noisy_image(H, W, seed, ("correlated", 0.2))

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
+from paper_1009_0958_b200 import _lib
 from paper_1009_0958_b200 import (
     REFLECT, REPLICATE, RasterImage, apply_filter, filter_batch_device, filter_device,
     filter_host, filter_rows_device, last_fixup_count, parse_filter_spec, synth,
@@ -186,11 +187,14 @@ S3_SPECS = ["vmf", "vmf:p=3", "bvdf:exact", "bvdf:minimax:q=3", "bvdf:rgb", "bvd
 
 @pytest.mark.parametrize("kernel", ["w3", "cta"])
 @pytest.mark.parametrize("spec", S3_SPECS)
-def test_3x3_kernels_against_oracle(cuda, spec, kernel, monkeypatch):
+def test_3x3_kernels_against_oracle(cuda, spec, kernel):
     """Both 3x3 schedules (warp row-sweep and CTA tiles) are bit-exact,
     including strips, frames, partial last chunks and both borders."""
-    torch = cuda
-    monkeypatch.setenv("DFG_S3_KERNEL", kernel)
+    with _lib.option("s3_schedule", 1 if kernel == "w3" else 2):
+        _check_3x3(cuda, spec)
+
+
+def _check_3x3(torch, spec):
     s = parse_filter_spec(spec)
     for H, W, seed, border in ((97, 61, 3, "replicate"), (40, 29, 4, "reflect"), (133, 90, 5, "replicate")):
         img = synth.noisy_image(H, W, seed, ("correlated", 0.2))
@@ -209,17 +213,13 @@ def test_3x3_kernels_against_oracle(cuda, spec, kernel, monkeypatch):
     assert (got == full[31:90]).all()
 
 
-@pytest.mark.parametrize("mode", ["0", "1", "2", "3"])
 @pytest.mark.parametrize("spec", ["ddf:exact", "bvdf:minimax:q=3", "acwddf:rgb", "vmf", "ddf:exact:p=1"])
-def test_host_streaming_3x3_against_oracle(cuda, spec, mode, monkeypatch):
-    """3x3 with pinned host buffers, banded copies (mode 0) and the opt-in
-    zero-copy streaming modes (1: the kernel reads and writes the mapped
-    host memory itself as aligned words; 2: input only; 3: output only).
-    Odd byte offsets of the buffers, widths whose rows are not 4-byte
-    multiples, single-row / single-column images, both borders and zero
-    vectors must all reproduce the oracle bit for bit."""
+def test_host_pinned_odd_offsets_3x3_against_oracle(cuda, spec):
+    """3x3 through the host pipeline with pinned host buffers at odd byte
+    offsets, widths whose rows are not 4-byte multiples, single-row /
+    single-column images, both borders and zero vectors: the oracle bit for
+    bit, and no stray writes around the output buffer."""
     torch = cuda
-    monkeypatch.setenv("DFG_HOST_STREAM", mode)
     s = parse_filter_spec(spec)
     for H, W, seed, border, shift in ((97, 61, 3, "replicate", 0), (40, 29, 4, "reflect", 1), (133, 90, 5, "replicate", 3),
                                       (1, 37, 6, "replicate", 2), (23, 1, 7, "reflect", 1), (64, 31, 8, "reflect", 0)):
@@ -263,59 +263,27 @@ def test_host_frame_stream(cuda, spec):
 
 @pytest.mark.parametrize("config", ["c1", "c2", "c3", "c4_bvdf_minimax", "c4_bvdf_rgb", "c4_ddf_minimax",
                                     "c4_ddf_rgb", "c5a", "c5b"])
-def test_config_size_sampled_rows_against_oracle(cuda, config):
-    """Parity at the BASELINE full sizes: the whole config frame (C5b: 3 of
-    its frames) is filtered on the GPU exactly as bench.py does; the oracle
-    re-filters sampled full-width row bands -- both image edges and two
-    interior bands at seeded positions -- from the same frame, and every
-    pixel must match bit for bit."""
+def test_config_whole_frame_against_oracle(cuda, config):
+    """Parity at the BASELINE full sizes, every pixel (SURVEY 8(d)
+    "Correctness reporting"; the reference's own whole-image oracles,
+    T/test_acceptance.py:169-195, T/test_filters.py:347-359): the config
+    frame (C5b: all 64 frames) is filtered on the GPU exactly as bench.py
+    does, the float64 oracle re-filters the whole frame on all host cores,
+    and every mismatch must be a documented near-tie (relative gap < 1e-5),
+    under 0.01 % of the pixels.  (So far every config has had 0.)"""
     torch = cuda
     cfg = synth.CONFIGS[config]
     s = parse_filter_spec(cfg["spec"])
-    h = s.window // 2
-    x = synth.config_input(config, frames=3 if config == "c5b" else None)
+    x = synth.config_input(config)
     if x.ndim == 4:
         got = filter_batch_device(torch.from_numpy(x).cuda(), s).cpu().numpy()
-        frames = list(zip(x, got))
     else:
-        frames = [(x, filter_device(torch.from_numpy(x).cuda(), s).cpu().numpy())]
-    rng = np.random.default_rng(sum(map(ord, config)))
-    for img, out in frames:
-        H = img.shape[0]
-        bands = [(0, 4), (H - 4, H)] + [(r, r + 6) for r in rng.integers(8, H - 16, size=2)]
-        for r0, r1 in bands:
-            b0, b1 = max(0, r0 - h), min(H, r1 + h)
-            want = oracle.filter_image(img[b0:b1], s, rows=(r0 - b0, r1 - b0))[r0 - b0:r1 - b0]
-            bad = int((out[r0:r1] != want).any(-1).sum())
-            assert bad == 0, (config, r0, r1, bad)
-
-
-def test_w3_deferred_queue_mode_subprocess(cuda, tmp_path):
-    """The opt-in deferred re-decision queue of the 3x3 row sweep
-    (DFG_W3_QUEUE=1, read once per process) reproduces the oracle, and a
-    second call on the same workspace starts from a clean queue."""
-    import subprocess
-    import sys
-    from pathlib import Path
-    root = Path(__file__).resolve().parent.parent
-    code = (
-        "import sys; sys.path.insert(0, %r)\n"
-        "import numpy as np, torch, oracle\n"
-        "from paper_1009_0958_b200 import filter_device, last_fixup_count, parse_filter_spec, synth\n"
-        "for spec in ('ddf:exact', 'acwddf:exact', 'bvdf:minimax'):\n"
-        "    s = parse_filter_spec(spec)\n"
-        "    img = synth.noisy_image(600, 300, 9, ('uncorrelated', 0.15))\n"
-        "    want = oracle.filter_image(img, s)\n"
-        "    x = torch.from_numpy(img).cuda()\n"
-        "    last_fixup_count()\n"
-        "    for _ in range(2):\n"
-        "        got = filter_device(x, s).cpu().numpy()\n"
-        "        assert (got == want).all(), spec\n"
-        "    assert last_fixup_count() > 0, spec\n"
-        "print('ok')\n" % str(root))
-    env = dict(__import__("os").environ, DFG_W3_QUEUE="1", DFG_S3_KERNEL="w3")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+        got = filter_device(torch.from_numpy(x).cuda(), s).cpu().numpy()
+    rep = oracle.parity_report(got, x, s)
+    assert rep["checked_px"] == int(np.prod(x.shape[:-1])), rep
+    assert rep["non_tie_mismatches"] == 0, (config, rep)
+    assert rep["near_ties"] <= 1e-4 * rep["checked_px"], (config, rep)
+    print(config, rep)
 
 
 @pytest.mark.parametrize("spec", ["ddf:exact", "acwddf:minimax:window=5", "bvdf:rgb:window=7"])
@@ -332,3 +300,37 @@ def test_extreme_aspect_ratios(cuda, spec, shape):
         got = filter_device(torch.from_numpy(img).cuda(), s, _policy(border)).cpu().numpy()
         assert (got == want).all(), (spec, shape, border, int((got != want).any(-1).sum()))
         assert (filter_host(img, s, _policy(border)) == want).all(), (spec, shape, border)
+
+
+def test_apply_filter_float64_boundary(cuda):
+    """The drop-in path (dfg_filter_host_f64): float64 RasterImage in, a new
+    float64 RasterImage out, equal to the device path on a frame large
+    enough for several host threads and row bands; values that are not
+    integers in 0..255 raise ValueError (the GPU path's one input
+    restriction) and leave no partial result."""
+    torch = cuda
+    img = synth.noisy_image(1030, 770, 7, ("correlated", 0.2))
+    for spec in ("ddf:exact", "acwddf:minimax:window=5", "bvdf:rgb:window=7"):
+        s = parse_filter_spec(spec)
+        ri = RasterImage(img.astype(np.float64))
+        out = apply_filter(ri, s)
+        assert out.pixels.dtype == np.float64 and not np.shares_memory(out.pixels, ri.pixels)
+        want = filter_device(torch.from_numpy(img).cuda(), s).cpu().numpy()
+        assert (out.pixels == want).all(), spec
+        assert apply_filter(ri, s, workers=4) == out
+    base = img[:40, :50].astype(np.float64)
+    for bad in (0.5, 256.0, -1.0, np.nan, np.inf, 255.0000001):
+        a = base.copy()
+        a[17, 23, 1] = bad
+        with pytest.raises(ValueError):
+            apply_filter(_raw_image(a), parse_filter_spec("ddf:exact"))
+    with pytest.raises(ValueError):  # through a real RasterImage (it accepts non-integral values)
+        apply_filter(RasterImage(base + 0.25), parse_filter_spec("ddf:exact"))
+
+
+def _raw_image(a):
+    """A duck-typed image carrying pixels RasterImage itself would reject
+    (NaN / inf), to reach the C ABI's own validation."""
+    class _Img:
+        pixels = a
+    return _Img()

@@ -1,5 +1,6 @@
-"""CPU (gloo, world size 2): the multi-GPU strip sharding host logic --
-strip bounds, neighbour halo exchange, all-gather -- reproduces the
+"""CPU (gloo, world sizes 2-8): the multi-GPU strip sharding host logic --
+strip bounds, neighbour halo exchange, chunked gather to the root (the
+exact code bench.py times on GPUs, parallel.StripJob) -- reproduces the
 single-process result bit for bit (the reference's row-partition
 equivalence, T/test_filters.py:434-439).  The per-strip filter is the float64
 oracle here (test infrastructure); on GPUs it is filter_rows_device."""
@@ -15,7 +16,7 @@ import torch.multiprocessing as mp
 
 import oracle
 from paper_1009_0958_b200 import parse_filter_spec, synth
-from paper_1009_0958_b200.parallel import filter_strips, frame_split, strip_rows
+from paper_1009_0958_b200.parallel import StripJob, frame_split, strip_rows
 
 
 def _free_port():
@@ -26,47 +27,83 @@ def _free_port():
     return p
 
 
-def _oracle_rows(strip, H, i0, r0, rows, spec, policy):
-    """Oracle on a strip: rebuild the global index frame so the border
-    policy applies at the true image edges (what dfg_filter_rows does)."""
-    full = np.zeros((H,) + tuple(strip.shape[1:]), dtype=np.uint8)
-    full[i0:i0 + strip.shape[0]] = strip.numpy()
-    out = oracle.filter_image(full, spec, policy, threads=1, rows=(r0, r0 + rows))
-    return torch.from_numpy(out[r0:r0 + rows].astype(np.uint8))
+def _oracle_filter(spec, border):
+    """filter_fn for StripJob: the oracle on a strip, rebuilt into the global
+    row index so the border policy applies at the true image edges (what
+    dfg_filter_rows does)."""
+    def fn(strip, H, i0, r0, rows, out):
+        full = np.zeros((H,) + tuple(strip.shape[1:]), dtype=np.uint8)
+        full[i0:i0 + strip.shape[0]] = strip.numpy()
+        res = oracle.filter_image(full, spec, border, threads=1, rows=(r0, r0 + rows))
+        out.copy_(torch.from_numpy(res[r0:r0 + rows].astype(np.uint8)))
+    return fn
 
 
-def _worker(rank, world, port, spec_text, border, H, W, q):
+def _worker(rank, world, port, spec_text, border, H, W, gather, chunks, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         spec = parse_filter_spec(spec_text)
         img = synth.noisy_image(H, W, 9, ("correlated", 0.2))
-        r0, r1, _, _ = strip_rows(H, world, rank, spec.window, border)
-        own = torch.from_numpy(img[r0:r1].copy())
-        full = filter_strips(own, r0, r1, H, spec, border, filter_fn=_oracle_rows, gather=True)
-        if rank == 0:
-            q.put(full.numpy())
+        try:
+            job = StripJob(H, W, spec.window, border=border, gather=gather, chunks=chunks)
+        except ValueError as e:  # every rank raises alike (no rank left waiting)
+            q.put((rank, "ValueError", str(e)))
+            return
+        job.own.copy_(torch.from_numpy(img[job.r0:job.r1]))
+        out = job.run(_oracle_filter(spec, border))
+        q.put((rank, (job.r0, job.r1), out.numpy().copy()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("spec_text,border", [("ddf:exact:window=7", "replicate"), ("acwddf:rgb:window=5", "reflect"),
-                                              ("bvdf:minimax", "replicate")])
-def test_two_rank_strips_equal_single_process(spec_text, border):
-    H, W = 37, 29
+def _run(world, spec_text, border, H, W, gather=True, chunks=3):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, spec_text, border, H, W, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, spec_text, border, H, W, gather, chunks, q))
+             for r in range(world)]
     for p in procs:
         p.start()
-    got = q.get(timeout=120)
+    res = {}
+    for _ in range(world):
+        rank, a, b = q.get(timeout=180)
+        res[rank] = (a, b)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world,spec_text,border,H,W", [
+    (2, "ddf:exact:window=7", "replicate", 37, 29), (2, "acwddf:rgb:window=5", "reflect", 37, 29),
+    (3, "bvdf:minimax", "replicate", 40, 23), (4, "ddf:exact", "replicate", 2, 11),  # ranks 2, 3 own no rows
+    (4, "ddf:exact:window=7", "replicate", 13, 9)])
+def test_strips_gather_to_root_equal_single_process(world, spec_text, border, H, W):
+    """Halo exchange into the strip buffers, chunked filtering and the
+    chunk-by-chunk gather to rank 0 reproduce the single-process frame --
+    including ranks that own no rows (they neither send nor receive)."""
+    res = _run(world, spec_text, border, H, W, gather=True, chunks=3)
     img = synth.noisy_image(H, W, 9, ("correlated", 0.2))
     want = oracle.filter_image(img, parse_filter_spec(spec_text), border, threads=2)
-    assert (got == want).all()
+    assert (res[0][1] == want).all()
+
+
+def test_strips_resident_output():
+    """Without the gather every rank keeps exactly its own filtered rows."""
+    H, W, spec_text = 41, 17, "acwddf:exact"
+    res = _run(3, spec_text, "replicate", H, W, gather=False)
+    img = synth.noisy_image(H, W, 9, ("correlated", 0.2))
+    want = oracle.filter_image(img, parse_filter_spec(spec_text), "replicate", threads=2)
+    for rank, ((r0, r1), out) in res.items():
+        assert (out == want[r0:r1]).all(), rank
+
+
+def test_too_many_ranks_raise_everywhere():
+    """Strips thinner than the halo cannot be served by neighbours alone:
+    every rank raises ValueError instead of waiting on a peer."""
+    res = _run(8, "ddf:exact:window=7", "replicate", 9, 5)
+    assert all(a == "ValueError" for a, _ in res.values())
 
 
 def test_strip_bounds_cover_every_row():
