@@ -44,10 +44,12 @@ def _headers_mtime() -> float:
 
 
 def build(verbose: bool = False, force: bool = False, jobs: int | None = None) -> Path:
-    nvcc = _nvcc()
-    OBJ.mkdir(exist_ok=True)
     sources = sorted(CSRC.glob("*.cu"))
     hdr = _headers_mtime()
+    if not force and LIB.exists() and LIB.stat().st_mtime >= max([hdr] + [s.stat().st_mtime for s in sources]):
+        return LIB  # up to date (e.g. the prebuilt library shipped to a GPU box without its objects)
+    nvcc = _nvcc()
+    OBJ.mkdir(exist_ok=True)
     todo = []
     for src in sources:
         obj = OBJ / (src.stem + ".o")

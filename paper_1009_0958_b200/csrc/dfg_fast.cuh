@@ -470,11 +470,23 @@ struct Cfg {
         return o;
     }
     static constexpr int NPL = (G == S) ? plane_off(S - 1) + ndv_of(S - 1) : NDV;  // planes resident at once
-    // 5x5 / 7x7: row-segment sums S_+du / S_-du (S values per pixel each)
+    // 5x5 / 7x7: row-segment sums S_+du (double-buffered: the next row
+    // offset's stage 1 writes one buffer while the outputs accumulate the
+    // other) and S_-du, S values per pixel each
     static constexpr bool SEG = S >= 5;
-    static constexpr int SEGN = SEG ? 2 * S : 0;
+    static constexpr int SEGN = SEG ? 3 * S : 0;
+    // 5x5 / 7x7 records: pair elements split by the parity of their first
+    // column (element e of a parity row holds columns c, c+1 with
+    // c = 2 (e - PADE) + parity), so a thread owning the pixel pair
+    // (2j, 2j+1) reads its partners -- all at even columns for du > 0, odd
+    // for du = 0 -- as consecutive 16-byte elements across the warp; the row
+    // pitch RWS2 = RW/2 + 8 keeps a warp's accesses bank-contiguous across
+    // row wraps
+    static constexpr int RW2 = RW / 2, PADE = H, RWS2 = RW2 + 8;
+    static constexpr int RECN2 = RH * RWS2;  // elements per parity array
+    static constexpr size_t kRecBytes = SEG ? (size_t)RECN2 * 64 : (size_t)RECN * 32;
     static constexpr size_t kSmem =
-        (size_t)RECN * 32 + (size_t)RN4 * 4 + (size_t)NPL * RN * sizeof(DT) + (size_t)SEGN * RN * sizeof(DT);
+        kRecBytes + (size_t)RN4 * 4 + (size_t)NPL * RN * sizeof(DT) + (size_t)SEGN * RN * sizeof(DT);
 };
 
 // One-pass first-strict-minimum with "best competitor of a different colour"
@@ -743,112 +755,220 @@ __device__ __forceinline__ void seg_sums(const DT (&T)[2 * S - 1], DT (&Sg)[S])
     for (int v = 1; v < S; v++) Sg[v] = dt_add(L[S - 1 - v], R[S - 1 - v]);
 }
 
-// 5x5 / 7x7 aggregation by row segments.  For row offset du, stage 1 evaluates
-// the pair planes D_(du,dv)(p) and, from the same registers, the pixel's
-// downward segment sums S_+du(p, v); after a barrier the upward sums
+// 5x5 / 7x7 aggregation by row segments.  For row offset du, stage 1
+// evaluates the pair planes D_(du,dv)(p) and, from the same registers, the
+// pixel's downward segment sums S_+du(p, v); after a barrier the upward sums
 // S_-du(q, v) are read off the planes (the pairs whose upper pixel is in the
 // row above); after a second barrier each output adds, for each window
 // candidate (u, v), S_+du(q, v) if u + du < S and S_-du(q, v) if u >= du:
 // agg(u, v) = sum_dy S_dy(q, v) covers every other window pixel exactly once.
 // s^3 segment loads per output instead of n(n-1)/2 pair loads (343 vs 1176
 // for 7x7), and the sums carry no cancellation.
+//
+// Schedule: a stage-1 item is a horizontal pixel PAIR (2j, 2j+1) against
+// partner elements (q, q+1) at even columns: both pixels' pair values come
+// from one element load (4 pairs per element, half the record traffic of
+// one pixel per item), and their plane / segment values leave as one
+// 16-byte store per plane.  The accumulation of row offset du - 1 runs in
+// the same barrier interval as stage 1 of du (S_+du is double-buffered;
+// the centre-column stash is read in phase 2, before the planes are
+// overwritten): two barriers per row offset instead of three, and the
+// accumulation fills the stage-1 load imbalance.
+template <typename DT>
+__device__ __forceinline__ void st_pair(DT *dst, DT a, DT b)  // dst 2-element aligned
+{
+    if constexpr (std::is_same<DT, float2>::value) {
+        *reinterpret_cast<float4 *>(dst) = make_float4(a.x, a.y, b.x, b.y);
+    } else {
+        *reinterpret_cast<float2 *>(dst) = make_float2(a, b);
+    }
+}
+
 template <int S, int FAM, int ST, int PC, int OPT, int TR, typename AG, typename CE, typename AA, typename AL>
-__device__ __forceinline__ void seg_stages(const float4 *sA, const float4 *sB, typename Cfg<S, FAM, OPT, TR>::DT *sD,
-                                           bool zchk, const KParams &kp, AG &ag, CE &cen, AA &aA, AL &aL)
+__device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FAM, OPT, TR>::DT *sD, bool zchk,
+                                           const KParams &kp, AG &ag, CE &cen, AA &aA, AL &aL)
 {
     using C = Cfg<S, FAM, OPT, TR>;
     using DT = typename C::DT;
-    constexpr int H = C::H, N = C::N, DC = C::DC, RW = C::RW, RH = C::RH, RN = C::RN, NT = C::NT;
-    constexpr int RWS = C::RWS, PADC = C::PADC, NDV = C::NDV;
+    constexpr int H = C::H, DC = C::DC, RW = C::RW, RH = C::RH, RN = C::RN, NT = C::NT;
+    constexpr int RW2 = C::RW2, RWS2 = C::RWS2, PADE = C::PADE, RECN2 = C::RECN2, NDV = C::NDV;
     constexpr bool CEN = C::CEN;
     constexpr bool BOTH = C::BOTH;
-    DT *sP = sD + C::NPL * RN;  // S_+du [v][RN]
-    DT *sM = sP + S * RN;       // S_-du [v][RN]
+    DT *sP0 = sD + C::NPL * RN;  // S_+du [v][RN], even du
+    DT *sP1 = sP0 + S * RN;      // S_+du [v][RN], odd du
+    DT *sM = sP1 + S * RN;       // S_-du [v][RN]
     const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    const float4 *recAe = rec, *recAo = rec + RECN2, *recBe = rec + 2 * RECN2, *recBo = rec + 3 * RECN2;
 
-    static_for<0, S>([&](auto du_c) {
+    auto to_dt = [](P2 da, P2 dl, bool hi) -> DT {
+        if constexpr (BOTH) return hi ? make_float2(hi2(da), hi2(dl)) : make_float2(lo2(da), lo2(dl));
+        else if constexpr (C::NEED_A) return hi ? hi2(da) : lo2(da);
+        else return hi ? hi2(dl) : lo2(dl);
+    };
+
+    // ---- stage 1 of row offset du: planes (+ downward segment sums) --------
+    auto stage1 = [&](auto du_c, auto zc_c) {
         constexpr int du = decltype(du_c)::value;
-        constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
-        constexpr int ndv = C::ndv_of(du);
-        constexpr int NK2 = (ndv + 1) / 2;
-        // ---- stage 1: planes (+ downward segment sums for du > 0) ---------
-        auto stage1 = [&](auto zc_c) {
-            constexpr bool ZC = decltype(zc_c)::value;
-            constexpr int items = (RH - du) * RW;
-            for (int it = tid; it < items; it += NT) {
-                const int py = it / RW, px = it - py * RW;
-                const int pidx = py * RWS + PADC + px;
-                const float4 a4 = lds_f4(sA + pidx), b4 = lds_f4(sB + pidx);
-                const Pix p = {a4.x, a4.z, b4.x, b4.z};
-                const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
-                const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
-                DT T[NDV];
-#pragma unroll
-                for (int kk = 0; kk < NK2; kk++) {
-                    const ulonglong2 A2 = lds_u2(qa + 2 * kk), B2 = lds_u2(qb + 2 * kk);
+        constexpr bool ZC = decltype(zc_c)::value;
+        constexpr int items = (RH - du) * RW2;
+        for (int it2 = tid; it2 < items; it2 += NT) {
+            const int py = it2 / RW2, j = it2 - py * RW2;
+            const int it0 = py * RW + 2 * j;
+            const int pe = py * RWS2 + PADE + j;  // the item's own element: pixels (2j, 2j+1)
+            const ulonglong2 pa = lds_u2(recAe + pe), pb = lds_u2(recBe + pe);
+            const Pix p0 = {lo2(P2{pa.x}), lo2(P2{pa.y}), lo2(P2{pb.x}), lo2(P2{pb.y})};
+            const Pix p1 = {hi2(P2{pa.x}), hi2(P2{pa.y}), hi2(P2{pb.x}), hi2(P2{pb.y})};
+            DT T0[NDV], T1[NDV];  // pair values of p0 / p1, t = offset - dv0 (fully unrolled)
+            if constexpr (du > 0) {
+                // partners at columns 2j + d, d = 2m - (S-1): p0 gets offsets
+                // d, d+1 (t = 2m, 2m+1), p1 gets d-1, d (t = 2m-1, 2m).
+                // Elements are visited right half first (m = H .. S-1:
+                // the prefix sums R of the segment sums), then left half
+                // descending (m = H-1 .. 0: the suffix sums L, each
+                // completing one segment sum), so only R and a value or two
+                // stay live -- the same operations and order as seg_sums.
+                const int qe = (py + du) * RWS2 + PADE + j - H;
+                DT R0[S], R1[S], L0, L1;
+                auto eval = [&](auto m_c) {
+                    constexpr int m = decltype(m_c)::value;
+                    const ulonglong2 A2 = lds_u2(recAe + qe + m), B2 = lds_u2(recBe + qe + m);
                     const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
-                    P2 da, dl;
-                    pair_values2<FAM, ST, PC, ZC>(p, q, kp, da, dl);
-                    DT v0, v1;
-                    if constexpr (BOTH) {
-                        v0 = make_float2(lo2(da), lo2(dl));
-                        v1 = make_float2(hi2(da), hi2(dl));
-                    } else if constexpr (C::NEED_A) {
-                        v0 = lo2(da);
-                        v1 = hi2(da);
-                    } else {
-                        v0 = lo2(dl);
-                        v1 = hi2(dl);
+                    P2 da0, dl0, da1, dl1;
+                    pair_values2<FAM, ST, PC, ZC>(p0, q, kp, da0, dl0);
+                    pair_values2<FAM, ST, PC, ZC>(p1, q, kp, da1, dl1);
+                    T0[2 * m] = to_dt(da0, dl0, false);
+                    if constexpr (m < S - 1) T0[2 * m + 1] = to_dt(da0, dl0, true);
+                    if constexpr (m > 0) T1[2 * m - 1] = to_dt(da1, dl1, false);
+                    T1[2 * m] = to_dt(da1, dl1, true);
+                };
+                static_for<H, S>([&](auto m_c) {  // right half, ascending t
+                    constexpr int m = decltype(m_c)::value;
+                    eval(m_c);
+                    // t = 2m-1 (m > H) and t = 2m are complete for both pixels
+                    if constexpr (m > H) st_pair(sD + (2 * m - 1) * RN + it0, T0[2 * m - 1], T1[2 * m - 1]);
+                    st_pair(sD + (2 * m) * RN + it0, T0[2 * m], T1[2 * m]);
+                    // prefix sums over t = S-1 .. : R[k] = sum of T[S-1 .. S-1+k]
+                    static_for<0, S>([&](auto k_c) {
+                        constexpr int k = decltype(k_c)::value, t = S - 1 + k;
+                        if constexpr (t == 2 * m || t == 2 * m - 1) {
+                            if constexpr (k == 0) {
+                                R0[0] = T0[t];
+                                R1[0] = T1[t];
+                            } else {
+                                R0[k] = dt_add(R0[k - 1], T0[t]);
+                                R1[k] = dt_add(R1[k - 1], T1[t]);
+                            }
+                        }
+                    });
+                });
+                DT *sPd = (du & 1) ? sP1 : sP0;
+                st_pair(sPd + it0, R0[S - 1], R1[S - 1]);  // v = 0: the whole right part
+                static_for<0, H>([&](auto mm_c) {           // left half, descending t
+                    constexpr int m = H - 1 - decltype(mm_c)::value;
+                    eval(std::integral_constant<int, m>{});
+                    // t = 2m+1 and t = 2m complete (t = 2m+1 = S-2 first)
+                    static_for<0, 2>([&](auto w_c) {
+                        constexpr int t = 2 * m + 1 - decltype(w_c)::value;
+                        st_pair(sD + t * RN + it0, T0[t], T1[t]);
+                        if constexpr (t == S - 2) {
+                            L0 = T0[t];
+                            L1 = T1[t];
+                        } else {
+                            L0 = dt_add(T0[t], L0);
+                            L1 = dt_add(T1[t], L1);
+                        }
+                        // L = L[t]: segment sum of the window in which the
+                        // pixel sits at column v = S-1-t
+                        st_pair(sPd + (S - 1 - t) * RN + it0, dt_add(L0, R0[t]), dt_add(L1, R1[t]));
+                    });
+                });
+            } else {
+                // same row, partners to the right: odd-column elements
+                // (2j+1+2m, 2j+2+2m); p0 offsets 2m+1, 2m+2, p1 offsets 2m,
+                // 2m+1 (plane k = offset - 1); each plane pair is stored as
+                // soon as both values exist
+                const int qe = py * RWS2 + PADE + j;
+                static_for<0, H + 1>([&](auto m_c) {
+                    constexpr int m = decltype(m_c)::value;
+                    const ulonglong2 A2 = lds_u2(recAo + qe + m), B2 = lds_u2(recBo + qe + m);
+                    const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
+                    P2 da0, dl0, da1, dl1;
+                    if constexpr (m < H) {
+                        pair_values2<FAM, ST, PC, ZC>(p0, q, kp, da0, dl0);
+                        T0[2 * m] = to_dt(da0, dl0, false);
+                        T0[2 * m + 1] = to_dt(da0, dl0, true);
                     }
-                    sD[(2 * kk) * RN + it] = v0;
-                    T[2 * kk] = v0;
-                    if (2 * kk + 1 < ndv) {
-                        sD[(2 * kk + 1) * RN + it] = v1;
-                        T[2 * kk + 1] = v1;
+                    pair_values2<FAM, ST, PC, ZC>(p1, q, kp, da1, dl1);
+                    if constexpr (m > 0) {
+                        T1[2 * m - 1] = to_dt(da1, dl1, false);
+                        st_pair(sD + (2 * m - 1) * RN + it0, T0[2 * m - 1], T1[2 * m - 1]);
                     }
-                }
-                if constexpr (du > 0) {  // here k = dv + S - 1 = t
-                    DT Sg[S];
-                    seg_sums<S>(T, Sg);
-#pragma unroll
-                    for (int v = 0; v < S; v++) sP[v * RN + it] = Sg[v];
-                }
-            }
-        };
-        if (zchk) stage1(std::true_type{});
-        else stage1(std::false_type{});
-        __syncthreads();
-        // ---- upward segment sums (du > 0) / both sides in the row (du = 0) --
-        {
-            constexpr int items = (RH - du) * RW;
-            for (int it = tid; it < items; it += NT) {
-                const int qi = it + du * RW;  // pixel q in rows du .. RH-1
-                DT T[NDV];
-                if constexpr (du == 0) {
-#pragma unroll
-                    for (int t = 0; t < NDV; t++) {
-                        const int dv = t - (S - 1);
-                        if (dv > 0) T[t] = sD[(dv - 1) * RN + qi];
-                        else if (dv < 0) T[t] = sD[(-dv - 1) * RN + qi + dv];
-                        else T[t] = dt_zero(DT());
+                    if constexpr (m < H) {
+                        T1[2 * m] = to_dt(da1, dl1, true);
+                        st_pair(sD + (2 * m) * RN + it0, T0[2 * m], T1[2 * m]);
                     }
-                } else {
-                    // T_q(-du, dv) = D_(du, -dv)(q + (-du, dv)): plane 2S-2-t
-#pragma unroll
-                    for (int t = 0; t < NDV; t++) {
-                        const int dv = t - (S - 1);
-                        T[t] = sD[(NDV - 1 - t) * RN + qi - du * RW + dv];
-                    }
-                }
-                DT Sg[S];
-                seg_sums<S>(T, Sg);
-                DT *dst = (du == 0) ? sP : sM;
-#pragma unroll
-                for (int v = 0; v < S; v++) dst[v * RN + qi] = Sg[v];
+                });
             }
         }
-        __syncthreads();
-        // ---- per-output accumulation of the segment sums --------------------
+    };
+    auto run_stage1 = [&](auto du_c) {
+        if (zchk) stage1(du_c, std::true_type{});
+        else stage1(du_c, std::false_type{});
+    };
+
+    // ---- phase 2 of du: upward sums (du > 0) / both sides in the row (du = 0),
+    // and the centre-column stash (read off the planes before stage 1 of
+    // du + 1 overwrites them) --------------------------------------------
+    auto phase2 = [&](auto du_c) {
+        constexpr int du = decltype(du_c)::value;
+        [[maybe_unused]] constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
+        constexpr int items = (RH - du) * RW;
+        for (int it = tid; it < items; it += NT) {
+            const int qi = it + du * RW;  // pixel q in rows du .. RH-1
+            DT T[NDV];
+            if constexpr (du == 0) {
+#pragma unroll
+                for (int t = 0; t < NDV; t++) {
+                    const int dv = t - (S - 1);
+                    if (dv > 0) T[t] = sD[(dv - 1) * RN + qi];
+                    else if (dv < 0) T[t] = sD[(-dv - 1) * RN + qi + dv];
+                    else T[t] = dt_zero(DT());
+                }
+            } else {
+                // T_q(-du, dv) = D_(du, -dv)(q + (-du, dv)): plane 2S-2-t
+#pragma unroll
+                for (int t = 0; t < NDV; t++) {
+                    const int dv = t - (S - 1);
+                    T[t] = sD[(NDV - 1 - t) * RN + qi - du * RW + dv];
+                }
+            }
+            DT Sg[S];
+            seg_sums<S>(T, Sg);
+            DT *dst = (du == 0) ? sP0 : sM;
+#pragma unroll
+            for (int v = 0; v < S; v++) dst[v * RN + qi] = Sg[v];
+        }
+        if constexpr (CEN) {  // centre-column stash: the pair (i, centre) itself
+#pragma unroll
+            for (int o = 0; o < OPT; o++) {
+                const int ry0 = ty * OPT + o;
+#pragma unroll
+                for (int i = 0; i < C::N; i++) {
+                    const int u = i / S, v = i % S;
+                    if (i < DC && H - u == du) {
+                        cen[o][i] = sD[(H - v - dv0) * RN + (ry0 + u) * RW + tx + v];
+                    } else if (i > DC && u - H == du) {
+                        cen[o][i] = sD[(v - H - dv0) * RN + (ry0 + H) * RW + tx + H];
+                    }
+                }
+            }
+        }
+    };
+
+    // ---- per-output accumulation of the segment sums of du ----------------
+    auto accumulate = [&](auto du_c) {
+        constexpr int du = decltype(du_c)::value;
+        const DT *sPd = (du & 1) ? sP1 : sP0;
 #pragma unroll
         for (int o = 0; o < OPT; o++) {
             const int ry0 = ty * OPT + o;
@@ -861,7 +981,7 @@ __device__ __forceinline__ void seg_stages(const float4 *sA, const float4 *sB, t
                     DT add = dt_zero(DT());
                     bool any = false;
                     if (u + du < S) {
-                        add = sP[v * RN + qi];
+                        add = sPd[v * RN + qi];
                         any = true;
                     }
                     if (du > 0 && u >= du) {
@@ -877,22 +997,25 @@ __device__ __forceinline__ void seg_stages(const float4 *sA, const float4 *sB, t
                             aL[o][i] += add;
                         }
                     }
-                    if constexpr (CEN) {  // centre-column stash: the pair (i, centre) itself
-                        if (i < DC && H - u == du) {
-                            const int dv = H - v;
-                            const int k = dv - dv0;
-                            cen[o][i] = sD[k * RN + qi];
-                        } else if (i > DC && u - H == du) {
-                            const int dv = v - H;
-                            const int k = dv - dv0;
-                            cen[o][i] = sD[k * RN + (ry0 + H) * RW + tx + H];
-                        }
-                    }
                 }
             }
         }
+    };
+
+    run_stage1(std::integral_constant<int, 0>{});
+    __syncthreads();
+    phase2(std::integral_constant<int, 0>{});
+    __syncthreads();
+    static_for<1, S>([&](auto du_c) {
+        constexpr int du = decltype(du_c)::value;
+        run_stage1(du_c);
+        accumulate(std::integral_constant<int, du - 1>{});
+        __syncthreads();
+        phase2(du_c);
         __syncthreads();
     });
+    accumulate(std::integral_constant<int, S - 1>{});
+    __syncthreads();
 }
 
 template <int S, int FAM, int ST, int PC, int OPT, int TR, int MINB>
@@ -909,7 +1032,8 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float4 *sA = reinterpret_cast<float4 *>(smem_raw);       // {gx_c, gx_c+1, gy_c, gy_c+1}
     float4 *sB = sA + C::RECN;                                // {gz_c, gz_c+1, aux_c, aux_c+1}
-    uint32_t *sK = reinterpret_cast<uint32_t *>(sB + C::RECN);  // packed colour (unpadded region)
+    // (5x5 / 7x7: the same elements in the parity layout, Cfg::RWS2)
+    uint32_t *sK = reinterpret_cast<uint32_t *>(smem_raw + C::kRecBytes);  // packed colour (unpadded region)
     DT *sD = reinterpret_cast<DT *>(sK + C::RN4);              // pair-distance planes
     __shared__ unsigned s_nflag;          // this CTA's pixels needing float64 re-decision
     __shared__ uint16_t s_flag[TH * 32];  // (window top row << 5) | column
@@ -958,14 +1082,28 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     // zero vectors (raw 0 vs gray-mapped 1) only matter to the Minkowski term
     const bool zany = __syncthreads_or(any_zero);  // also the pass-1 barrier
     const bool zchk = C::NEED_L && zany;
-    for (int idx = tid; idx < C::RECN; idx += NT) {
-        const int ry = idx / RWS, c = idx - ry * RWS;
-        const int r0 = c - PADC, r1 = r0 + 1;
-        const float4 neutral = make_float4(1.f, 1.f, 1.f, pad_aux);
-        const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
-        const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
-        sA[idx] = make_float4(f.x, s.x, f.y, s.y);
-        sB[idx] = make_float4(f.z, s.z, f.w, s.w);
+    const float4 neutral = make_float4(1.f, 1.f, 1.f, pad_aux);
+    if constexpr (C::SEG) {
+        // parity layout: element e of parity row (par, ry) = columns c, c+1,
+        // c = 2 (e - PADE) + par; arrays A-even, A-odd, B-even, B-odd
+        for (int idx = tid; idx < 2 * C::RECN2; idx += NT) {
+            const int par = idx >= C::RECN2 ? 1 : 0, k = idx - par * C::RECN2;
+            const int ry = k / C::RWS2, e = k - ry * C::RWS2;
+            const int r0 = 2 * (e - C::PADE) + par, r1 = r0 + 1;
+            const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
+            const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
+            sA[idx] = make_float4(f.x, s.x, f.y, s.y);
+            sA[2 * C::RECN2 + idx] = make_float4(f.z, s.z, f.w, s.w);
+        }
+    } else {
+        for (int idx = tid; idx < C::RECN; idx += NT) {
+            const int ry = idx / RWS, c = idx - ry * RWS;
+            const int r0 = c - PADC, r1 = r0 + 1;
+            const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
+            const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
+            sA[idx] = make_float4(f.x, s.x, f.y, s.y);
+            sB[idx] = make_float4(f.z, s.z, f.w, s.w);
+        }
     }
     __syncthreads();
 
@@ -988,7 +1126,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     }
 
     if constexpr (C::SEG) {
-        seg_stages<S, FAM, ST, PC, OPT, TR>(sA, sB, sD, zchk, kp, ag, cen, aA, aL);
+        seg_stages<S, FAM, ST, PC, OPT, TR>(sA, sD, zchk, kp, ag, cen, aA, aL);
     } else
     static_for<0, S / C::G>([&](auto g_c) {
         constexpr int g0 = decltype(g_c)::value * C::G;
