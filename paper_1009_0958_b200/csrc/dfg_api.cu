@@ -1,6 +1,8 @@
 // dfg_api.cu -- C ABI (include/dirfilt_gpu.h) over the directional filter
 // kernels: validation (the reference's ValueError cases), parameter
 // packing, the FP32 decision launch and the float64 re-decision launch.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdio.h>
@@ -20,6 +22,31 @@ Options &options()
 {
     static Options o;
     return o;
+}
+
+bool encode_rows_map(CUtensorMap *map, const void *base, long long row_bytes, int rows, int frames, long long pitch,
+                     long long fstride, const int box[3])
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            fn = nullptr;
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode || !base) return false;
+    if (((uintptr_t)base & 15) || (pitch & 15) || (frames > 1 && (fstride & 15))) return false;
+    if (row_bytes < 16 || rows < 1 || frames < 1 || pitch >= (1LL << 40) || fstride >= (1LL << 40)) return false;
+    const cuuint64_t dims[3] = {(cuuint64_t)row_bytes, (cuuint64_t)rows, (cuuint64_t)frames};
+    const cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)(frames > 1 ? fstride : pitch * rows)};
+    const cuuint32_t bx[3] = {(cuuint32_t)box[0], (cuuint32_t)box[1], (cuuint32_t)box[2]};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void *>(base), dims, strides, bx, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int sm_count(int dev)
@@ -294,6 +321,8 @@ int dfg_set_option(int32_t key, double value)
     case DFG_OPT_W3_RPC: o.w3_rpc = v; break;
     case DFG_OPT_W3_SMALL_WPS: o.w3_small_wps = v; break;
     case DFG_OPT_CR_MARGIN: o.cr_margin = value; break;
+    case DFG_OPT_TMA: o.tma = v; break;
+    case DFG_OPT_PERSIST: o.persist = v; break;
     default: return fail(DFG_E_ARG, "unknown option key");
     }
     g_host.drop_graphs();  // captured pipelines bake the old settings in
@@ -314,6 +343,8 @@ double dfg_get_option(int32_t key)
     case DFG_OPT_W3_RPC: return o.w3_rpc;
     case DFG_OPT_W3_SMALL_WPS: return o.w3_small_wps;
     case DFG_OPT_CR_MARGIN: return o.cr_margin;
+    case DFG_OPT_TMA: return o.tma;
+    case DFG_OPT_PERSIST: return o.persist;
     default: return NAN;
     }
 }

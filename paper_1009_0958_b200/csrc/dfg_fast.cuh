@@ -33,6 +33,8 @@
 // acosf(dot * rsqrt * rsqrt) loses ~1% of decisions.
 #pragma once
 
+#include <cuda.h>
+
 #include <type_traits>
 
 #include "dfg_f64.cuh"
@@ -483,10 +485,24 @@ struct Cfg {
     // pitch RWS2 = RW/2 + 8 keeps a warp's accesses bank-contiguous across
     // row wraps
     static constexpr int RW2 = RW / 2, PADE = H, RWS2 = RW2 + 8;
+    // stage-1 items: horizontal pixel pairs (half the record loads) where
+    // the register budget allows their live set (>= 168 per thread: the
+    // 1-CTA-per-SM shapes); one pixel per item otherwise
+    static constexpr bool ITEM2 = NT * 168 <= 65536;
     static constexpr int RECN2 = RH * RWS2;  // elements per parity array
     static constexpr size_t kRecBytes = SEG ? (size_t)RECN2 * 64 : (size_t)RECN * 32;
-    static constexpr size_t kSmem =
+    // TMA buffers (128-byte aligned): two raw uint8 regions (box of 144 bytes
+    // x RH rows: a tile load must start at a 16-byte aligned column, so the
+    // box starts up to 15 bytes left of the region) and the tile's output
+    // colours (TH rows x 96 bytes)
+    static constexpr int kRawPitch = 144, kRawBytes = RH * kRawPitch, kRawBuf = (kRawBytes + 127) & ~127;
+    static_assert(3 * RW + 15 <= kRawPitch, "region row fits the TMA box");
+    static constexpr size_t kBodyBytes =
         kRecBytes + (size_t)RN4 * 4 + (size_t)NPL * RN * sizeof(DT) + (size_t)SEGN * RN * sizeof(DT);
+    static constexpr size_t kRawOff = (kBodyBytes + 127) & ~(size_t)127;
+    static constexpr size_t kOutOff = kRawOff + 2 * (size_t)kRawBuf;
+    static constexpr int kOutBuf = (TH * 96 + 127) & ~127;  // double-buffered (tile parity)
+    static constexpr size_t kSmem = kOutOff + 2 * (size_t)kOutBuf + 128;  // + 128: runtime base alignment
 };
 
 // One-pass first-strict-minimum with "best competitor of a different colour"
@@ -769,11 +785,15 @@ __device__ __forceinline__ void seg_sums(const DT (&T)[2 * S - 1], DT (&Sg)[S])
 // partner elements (q, q+1) at even columns: both pixels' pair values come
 // from one element load (4 pairs per element, half the record traffic of
 // one pixel per item), and their plane / segment values leave as one
-// 16-byte store per plane.  The accumulation of row offset du - 1 runs in
-// the same barrier interval as stage 1 of du (S_+du is double-buffered;
-// the centre-column stash is read in phase 2, before the planes are
-// overwritten): two barriers per row offset instead of three, and the
-// accumulation fills the stage-1 load imbalance.
+// 16-byte store per plane.  Two barrier intervals per row offset: stage 1
+// of du runs beside the outputs' accumulation of du - 1 (FP32-heavy item
+// work next to shared-memory-heavy accumulation, which also fills the item
+// loop's load imbalance; S_+du is double-buffered), then phase 2 of du.
+// The row's own sums (du = 0) go to the S_- buffer; the centre-column
+// stash is read in phase 2, before stage 1 of du + 1 overwrites the
+// planes.  (Measured: pairing phase 2 with the S_+ half of the
+// accumulation instead -- no double buffer -- ran 9 % slower on C5a: both
+// halves of each pairing then contend for the same pipe.)
 template <typename DT>
 __device__ __forceinline__ void st_pair(DT *dst, DT a, DT b)  // dst 2-element aligned
 {
@@ -786,7 +806,7 @@ __device__ __forceinline__ void st_pair(DT *dst, DT a, DT b)  // dst 2-element a
 
 template <int S, int FAM, int ST, int PC, int OPT, int TR, typename AG, typename CE, typename AA, typename AL>
 __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FAM, OPT, TR>::DT *sD, bool zchk,
-                                           const KParams &kp, AG &ag, CE &cen, AA &aA, AL &aL)
+                                           const KParams &kp, AG &ag, CE &cen, AA &aA, AL &aL, const int tid)
 {
     using C = Cfg<S, FAM, OPT, TR>;
     using DT = typename C::DT;
@@ -796,8 +816,8 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
     constexpr bool BOTH = C::BOTH;
     DT *sP0 = sD + C::NPL * RN;  // S_+du [v][RN], even du
     DT *sP1 = sP0 + S * RN;      // S_+du [v][RN], odd du
-    DT *sM = sP1 + S * RN;       // S_-du [v][RN]
-    const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+    DT *sM = sP1 + S * RN;       // S_-du [v][RN] (du = 0: both sides in the row)
+    const int tx = tid & 31, ty = tid >> 5;
     const float4 *recAe = rec, *recAo = rec + RECN2, *recBe = rec + 2 * RECN2, *recBo = rec + 3 * RECN2;
 
     auto to_dt = [](P2 da, P2 dl, bool hi) -> DT {
@@ -911,9 +931,57 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
             }
         }
     };
+    // one-pixel items (register-tight shapes, Cfg::ITEM2 false): pixel p at
+    // column c against the pair elements of c's parity, (q, q+1) at c - (S-1)
+    // + 2m (du > 0) or c + 1 + 2m (du = 0, the other parity)
+    auto stage1_px = [&](auto du_c, auto zc_c) {
+        constexpr int du = decltype(du_c)::value;
+        constexpr bool ZC = decltype(zc_c)::value;
+        constexpr int items = (RH - du) * RW;
+        constexpr int ndv = C::ndv_of(du);
+        constexpr int NK2 = (ndv + 1) / 2;
+        for (int it = tid; it < items; it += NT) {
+            const int py = it / RW, c = it - py * RW;
+            const int par = c & 1, e = (c >> 1) + PADE;
+            const float4 *pA = par ? recAo : recAe, *pB = par ? recBo : recBe;
+            const float4 a4 = lds_f4(pA + py * RWS2 + e), b4 = lds_f4(pB + py * RWS2 + e);
+            const Pix p = {a4.x, a4.z, b4.x, b4.z};
+            // partner elements: du > 0 same parity, from e - H; du = 0 the
+            // other parity (element of column c + 1 = c + 1's own index)
+            const float4 *qA = (du > 0) ? pA : (par ? recAe : recAo);
+            const float4 *qB = (du > 0) ? pB : (par ? recBe : recBo);
+            const int qe = (py + du) * RWS2 + ((du > 0) ? e - H : ((c + 1) >> 1) + PADE);
+            DT T[NDV];
+#pragma unroll
+            for (int kk = 0; kk < NK2; kk++) {
+                const ulonglong2 A2 = lds_u2(qA + qe + kk), B2 = lds_u2(qB + qe + kk);
+                const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
+                P2 da, dl;
+                pair_values2<FAM, ST, PC, ZC>(p, q, kp, da, dl);
+                T[2 * kk] = to_dt(da, dl, false);
+                sD[(2 * kk) * RN + it] = T[2 * kk];
+                if (2 * kk + 1 < ndv) {
+                    T[2 * kk + 1] = to_dt(da, dl, true);
+                    sD[(2 * kk + 1) * RN + it] = T[2 * kk + 1];
+                }
+            }
+            if constexpr (du > 0) {
+                DT Sg[S];
+                seg_sums<S>(T, Sg);
+                DT *sPd = (du & 1) ? sP1 : sP0;
+#pragma unroll
+                for (int v = 0; v < S; v++) sPd[v * RN + it] = Sg[v];
+            }
+        }
+    };
     auto run_stage1 = [&](auto du_c) {
-        if (zchk) stage1(du_c, std::true_type{});
-        else stage1(du_c, std::false_type{});
+        if constexpr (C::ITEM2) {
+            if (zchk) stage1(du_c, std::true_type{});
+            else stage1(du_c, std::false_type{});
+        } else {
+            if (zchk) stage1_px(du_c, std::true_type{});
+            else stage1_px(du_c, std::false_type{});
+        }
     };
 
     // ---- phase 2 of du: upward sums (du > 0) / both sides in the row (du = 0),
@@ -944,7 +1012,7 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
             }
             DT Sg[S];
             seg_sums<S>(T, Sg);
-            DT *dst = (du == 0) ? sP0 : sM;
+            DT *dst = sM;
 #pragma unroll
             for (int v = 0; v < S; v++) dst[v * RN + qi] = Sg[v];
         }
@@ -965,7 +1033,8 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
         }
     };
 
-    // ---- per-output accumulation of the segment sums of du ----------------
+    // ---- per-output accumulation of the segment sums of du: S_+du
+    // (u + du < S) and S_-du (u >= du; du = 0: the row's both-sided sums) --
     auto accumulate = [&](auto du_c) {
         constexpr int du = decltype(du_c)::value;
         const DT *sPd = (du & 1) ? sP1 : sP0;
@@ -979,23 +1048,23 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
                     const int i = u * S + v;
                     const int qi = (ry0 + u) * RW + tx + v;
                     DT add = dt_zero(DT());
-                    bool any = false;
-                    if (u + du < S) {
+                    if (du == 0) {
+                        add = sM[v * RN + qi];
+                    } else if (u + du < S && u >= du) {
+                        add = dt_add(sPd[v * RN + qi], sM[v * RN + qi]);
+                    } else if (u + du < S) {
                         add = sPd[v * RN + qi];
-                        any = true;
+                    } else if (u >= du) {
+                        add = sM[v * RN + qi];
+                    } else {
+                        continue;
                     }
-                    if (du > 0 && u >= du) {
-                        add = any ? dt_add(add, sM[v * RN + qi]) : sM[v * RN + qi];
-                        any = true;
-                    }
-                    if (any) {
-                        if constexpr (BOTH) {
-                            ag[o][i] = add2(ag[o][i], *reinterpret_cast<const P2 *>(&add));
-                        } else if constexpr (C::NEED_A) {
-                            aA[o][i] += add;
-                        } else {
-                            aL[o][i] += add;
-                        }
+                    if constexpr (BOTH) {
+                        ag[o][i] = add2(ag[o][i], *reinterpret_cast<const P2 *>(&add));
+                    } else if constexpr (C::NEED_A) {
+                        aA[o][i] += add;
+                    } else {
+                        aL[o][i] += add;
                     }
                 }
             }
@@ -1018,9 +1087,58 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
     __syncthreads();
 }
 
+// ---- TMA helpers (raw PTX; sm_90+ bulk tensor copies, mbarrier completion) --
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
+{
+    uint32_t done;
+    do {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done)
+                     : "r"(smem_u32(bar)), "r"(phase)
+                     : "memory");
+    } while (!done);
+}
+// one thread: region rows of a tile -> shared memory, completion on `bar`
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar,
+                                            uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap *map, int c0, int c1, int c2, const void *src)
+{
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// at most one bulk store group (the previous tile's) still reading its source
+__device__ __forceinline__ void tma_store_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Persistent CTA kernel: each CTA walks tiles blockIdx.x, + gridDim.x, ...
+// (x fastest, then tile rows, then frames).  Interior tiles of a
+// TMA-eligible image (KParams::tma_in) receive their uint8 region by one
+// bulk tensor copy issued while the CTA still works on the previous tile
+// (double-buffered raw region, mbarrier completion); border tiles resolve
+// the border policy with indexed loads.  The selected colours of a tile are
+// assembled in shared memory (float64 re-decisions included) and leave as
+// one bulk tensor store (KParams::tma_out; the tensor map clips partial
+// tiles at the image edge), else as byte stores.
 template <int S, int FAM, int ST, int PC, int OPT, int TR, int MINB>
 __global__ void __launch_bounds__(TR * 32, MINB)
-dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const KParams kp)
+dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const __grid_constant__ KParams kp)
 {
     using C = Cfg<S, FAM, OPT, TR>;
     using DT = typename C::DT;
@@ -1029,327 +1147,460 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
     constexpr bool CEN = C::CEN;
     constexpr bool BOTH = C::BOTH;
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     float4 *sA = reinterpret_cast<float4 *>(smem_raw);       // {gx_c, gx_c+1, gy_c, gy_c+1}
     float4 *sB = sA + C::RECN;                                // {gz_c, gz_c+1, aux_c, aux_c+1}
     // (5x5 / 7x7: the same elements in the parity layout, Cfg::RWS2)
     uint32_t *sK = reinterpret_cast<uint32_t *>(smem_raw + C::kRecBytes);  // packed colour (unpadded region)
-    DT *sD = reinterpret_cast<DT *>(sK + C::RN4);              // pair-distance planes
-    __shared__ unsigned s_nflag;          // this CTA's pixels needing float64 re-decision
+    DT *sD = reinterpret_cast<DT *>(sK + C::RN4);              // pair-distance planes (+ segment sums)
+    // (the dynamic window's base is only guaranteed 16-byte aligned)
+    uint8_t *abase = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    uint8_t *sRaw = abase + C::kRawOff;  // [2][RH][kRawPitch] TMA region buffers
+    uint8_t *sOut0 = abase + C::kOutOff;  // [2][TH][96] the tile's output colours (by tile parity)
+    __shared__ unsigned s_nflag;          // this tile's pixels needing float64 re-decision
     __shared__ uint16_t s_flag[TH * 32];  // (window top row << 5) | column
     __shared__ int s_b;
     __shared__ bool s_close;
+    __shared__ __align__(8) uint64_t s_bar[2];
+    // per-tile state kept in shared memory rather than in registers live
+    // across the tile loop (the unrolled stages need every register):
+    // s_tile[parity] = {x0, y0, frame, inside} of the tile using raw buffer
+    // `parity`; s_state bit 0 = this tile's parity, bits 1, 2 = mbarrier
+    // phases of the two buffers
+    __shared__ int s_tile[2][4];
+    __shared__ uint32_t s_state;
 
-    const int tid = threadIdx.x;
-    const int tx = tid & 31, ty = tid >> 5;
-    const int tile_x0 = blockIdx.x * 32, tile_y0 = blockIdx.y * TH;
-    const int frame = blockIdx.z;
-    const uint8_t *fin = in + (long long)frame * kp.in_fstride;
-    if (tid == 0) s_nflag = 0;
-
-    // ---- stage 0: region staging + per-pixel normalisation ----------------
-    // Pass 1 normalises every region pixel into a temporary float4 record
-    // (in the plane buffer, free at this point); pass 2 assembles the pair
-    // elements (c, c+1) with whole 16-byte stores.  Pad positions hold a
-    // neutral gray pixel; tiles inside the image skip the border resolution.
-    float4 *tmp = reinterpret_cast<float4 *>(sD);
-    static_assert((size_t)C::NPL * RN * sizeof(DT) >= (size_t)RN * sizeof(float4), "staging temp fits");
+    // (tile counts are recomputed from kp where needed: every register live
+    // across the tile loop is taken from the unrolled stages' budget)
+    auto n_tiles = [&]() { return ((kp.W + 31) / 32) * ((kp.out_rows + TH - 1) / TH) * kp.n_frames; };
     const float pad_aux = (ST == ST_MINIMAX) ? 0.57735026f : (ST == ST_CHROMA ? (1.f / 3.f) : 1.7320508f);
-    const int gy_top = kp.out_row0 + tile_y0 - H;  // global row of region row 0
-    const bool inside = gy_top >= kp.in_row0 && gy_top + RH <= kp.in_row0 + kp.in_rows &&
-                        gy_top >= 0 && gy_top + RH <= kp.global_H && tile_x0 - H >= 0 && tile_x0 - H + RW <= kp.W;
-    bool any_zero = false;
-    for (int idx = tid; idx < RN; idx += NT) {
-        const int ry = idx / RW, rx = idx - ry * RW;
-        int gyy, gxx;
-        if (inside) {
-            gyy = gy_top + ry - kp.in_row0;
-            gxx = tile_x0 - H + rx;
-        } else {
-            gyy = resolve_idx(gy_top + ry, kp.global_H, kp.border) - kp.in_row0;
-            gyy = min(max(gyy, 0), kp.in_rows - 1);
-            gxx = resolve_idx(tile_x0 + rx - H, kp.W, kp.border);
-        }
-        const uint8_t *px = fin + (long long)gyy * kp.in_pitch + gxx * 3;
-        const uint32_t r8 = px[0], g8 = px[1], b8 = px[2];
-        const bool zero = (r8 | g8 | b8) == 0;
-        any_zero |= zero;
-        const float gx = zero ? 1.f : (float)r8, gy = zero ? 1.f : (float)g8, gz = zero ? 1.f : (float)b8;
-        const float aux = encode_aux<ST, C::NEED_L>(gx, gy, gz, zero);
-        sK[idx] = r8 | (g8 << 8) | (b8 << 16);
-        tmp[idx] = make_float4(gx, gy, gz, aux);
-    }
-    // zero vectors (raw 0 vs gray-mapped 1) only matter to the Minkowski term
-    const bool zany = __syncthreads_or(any_zero);  // also the pass-1 barrier
-    const bool zchk = C::NEED_L && zany;
     const float4 neutral = make_float4(1.f, 1.f, 1.f, pad_aux);
-    if constexpr (C::SEG) {
-        // parity layout: element e of parity row (par, ry) = columns c, c+1,
-        // c = 2 (e - PADE) + par; arrays A-even, A-odd, B-even, B-odd
-        for (int idx = tid; idx < 2 * C::RECN2; idx += NT) {
-            const int par = idx >= C::RECN2 ? 1 : 0, k = idx - par * C::RECN2;
-            const int ry = k / C::RWS2, e = k - ry * C::RWS2;
-            const int r0 = 2 * (e - C::PADE) + par, r1 = r0 + 1;
-            const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
-            const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
-            sA[idx] = make_float4(f.x, s.x, f.y, s.y);
-            sA[2 * C::RECN2 + idx] = make_float4(f.z, s.z, f.w, s.w);
+
+    struct Tile {
+        int x0, y0, frame, gy_top;
+        bool inside;
+    };
+    // t / d for t < 2^24 by a float reciprocal and two correction steps
+    // (a few instructions instead of an integer division per tile)
+    auto divmod = [](int t, int d, int &q) {
+        q = __float2int_rz(__int2float_rn(t) * __frcp_rn(__int2float_rn(d)));
+        int r = t - q * d;
+#pragma unroll
+        for (int k = 0; k < 2; k++) {  // |error| <= 2 below 2^24
+            if (r < 0) { q--; r += d; }
+            if (r >= d) { q++; r -= d; }
         }
-    } else {
-        for (int idx = tid; idx < C::RECN; idx += NT) {
-            const int ry = idx / RWS, c = idx - ry * RWS;
-            const int r0 = c - PADC, r1 = r0 + 1;
-            const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
-            const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
-            sA[idx] = make_float4(f.x, s.x, f.y, s.y);
-            sB[idx] = make_float4(f.z, s.z, f.w, s.w);
+        return r;
+    };
+    auto tile_of = [&](int t) {
+        const int tiles_x = (kp.W + 31) / 32, tiles_y = (kp.out_rows + TH - 1) / TH;
+        Tile T;
+        int r, f;
+        T.x0 = divmod(t, tiles_x, r) * 32;
+        T.y0 = divmod(r, tiles_y, f) * TH;
+        T.frame = f;
+        T.gy_top = kp.out_row0 + T.y0 - H;  // global row of region row 0
+        T.inside = T.gy_top >= kp.in_row0 && T.gy_top + RH <= kp.in_row0 + kp.in_rows && T.gy_top >= 0 &&
+                   T.gy_top + RH <= kp.global_H && T.x0 - H >= 0 && T.x0 - H + RW <= kp.W;
+        return T;
+    };
+    auto issue_load = [&](const Tile &T, int buf) {  // one thread
+        // (the box start column must be 16-byte aligned: the region starts
+        // (3 (x0 - H)) & 15 bytes into the box)
+        tma_load_3d(sRaw + buf * C::kRawBuf, &kp.tm_in, (3 * (T.x0 - H)) & ~15, T.gy_top - kp.in_row0, T.frame,
+                    &s_bar[buf], C::kRawBytes);
+    };
+    auto publish = [&](const Tile &T, int par) {  // one thread
+        s_tile[par][0] = T.x0;
+        s_tile[par][1] = T.y0;
+        s_tile[par][2] = T.frame;
+        s_tile[par][3] = T.inside;
+    };
+    int t = blockIdx.x;
+    if (threadIdx.x == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        s_state = 0u;
+        if (t < n_tiles()) {
+            const Tile T0 = tile_of(t);
+            publish(T0, 0);
+            if (T0.inside && kp.tma_in) issue_load(T0, 0);
         }
     }
     __syncthreads();
+#pragma unroll 1
+    for (; t < n_tiles(); t += gridDim.x) {
+        // the thread index re-read per tile (volatile): keeps the compiler
+        // from hoisting every tid-derived shared-memory address of the
+        // unrolled stages out of the tile loop (hundreds of live registers)
+        int tid, tx, ty;
+        asm volatile("mov.u32 %0, %%tid.x;" : "=r"(tid));
+        __builtin_assume(tid >= 0 && tid < NT);  // (the range stays known)
+        tx = tid & 31;
+        ty = tid >> 5;
+        const uint32_t par = s_state & 1u;
+        Tile T;
+        T.x0 = s_tile[par][0];
+        T.y0 = s_tile[par][1];
+        T.frame = s_tile[par][2];
+        T.inside = s_tile[par][3] != 0;
+        T.gy_top = kp.out_row0 + T.y0 - H;
+        const int tile_x0 = T.x0, frame = T.frame;
+        if (tid == 0) s_nflag = 0;
 
-    // aggregates: BOTH -> packed (angular, Minkowski) pairs; else scalars
-    P2 ag[OPT][BOTH ? N : 1];
-    DT cen[OPT][CEN ? N : 1];  // centre column (angular, Minkowski) or (Minkowski)
-    float aA[OPT][(C::NEED_A && !BOTH) ? N : 1], aL[OPT][(C::NEED_L && !BOTH) ? N : 1];
-#pragma unroll
-    for (int o = 0; o < OPT; o++) {
-#pragma unroll
-        for (int i = 0; i < N; i++) {
-            if constexpr (BOTH) ag[o][i] = pk2(kp.self_term, 0.f);
-            else if constexpr (C::NEED_A) aA[o][i] = kp.self_term;
-            else aL[o][i] = 0.f;
+        // ---- stage 0: region staging + per-pixel normalisation ------------
+        // Pass 1 normalises every region pixel into a temporary float4
+        // record (in the plane buffer, free at this point); pass 2 assembles
+        // the pair elements (c, c+1) with whole 16-byte stores.  Pad
+        // positions hold a neutral gray pixel.
+        float4 *tmp = reinterpret_cast<float4 *>(sD);
+        static_assert((size_t)C::NPL * RN * sizeof(DT) >= (size_t)RN * sizeof(float4), "staging temp fits");
+        const bool from_tma = kp.tma_in && T.inside;
+        bool any_zero = false;
+        auto norm = [&](int idx, uint32_t r8, uint32_t g8, uint32_t b8) {
+            const bool zero = (r8 | g8 | b8) == 0;
+            any_zero |= zero;
+            const float gx = zero ? 1.f : (float)r8, gy = zero ? 1.f : (float)g8, gz = zero ? 1.f : (float)b8;
+            const float aux = encode_aux<ST, C::NEED_L>(gx, gy, gz, zero);
+            sK[idx] = r8 | (g8 << 8) | (b8 << 16);
+            tmp[idx] = make_float4(gx, gy, gz, aux);
+        };
+        // the bulk store of two tiles ago (same parity) has read its sOut buffer
+        if (tid == 0 && kp.tma_out) tma_store_wait_read1();
+        if (from_tma) {  // the region from shared memory (its bulk copy was issued a tile ago)
+            const uint32_t st = s_state;
+            mbar_wait(&s_bar[par], (st >> (1 + par)) & 1u);
+            const uint8_t *raw = sRaw + par * C::kRawBuf + ((3 * (tile_x0 - H)) & 15);
+            for (int idx = tid; idx < RN; idx += NT) {
+                const int ry = idx / RW, rx = idx - ry * RW;
+                const uint8_t *px = raw + ry * C::kRawPitch + 3 * rx;
+                norm(idx, px[0], px[1], px[2]);
+            }
+        } else {  // indexed loads, border policy by index resolution
+            const uint8_t *fin = in + (long long)frame * kp.in_fstride;
+            for (int idx = tid; idx < RN; idx += NT) {
+                const int ry = idx / RW, rx = idx - ry * RW;
+                int gyy, gxx;
+                if (T.inside) {
+                    gyy = T.gy_top + ry - kp.in_row0;
+                    gxx = tile_x0 - H + rx;
+                } else {
+                    gyy = resolve_idx(T.gy_top + ry, kp.global_H, kp.border) - kp.in_row0;
+                    gyy = min(max(gyy, 0), kp.in_rows - 1);
+                    gxx = resolve_idx(tile_x0 + rx - H, kp.W, kp.border);
+                }
+                const uint8_t *px = fin + (long long)gyy * kp.in_pitch + gxx * 3;
+                norm(idx, px[0], px[1], px[2]);
+            }
         }
-        if constexpr (CEN) {
-            if constexpr (BOTH) cen[o][DC] = make_float2(kp.self_term, 0.f);
-            else cen[o][DC] = dt_zero(DT());
+        // zero vectors (raw 0 vs gray-mapped 1) only matter to the Minkowski term
+        const bool zany = __syncthreads_or(any_zero);  // also the pass-1 barrier
+        const bool zchk = C::NEED_L && zany;
+        // the next tile's region streams in while this one is computed (its
+        // buffer was last read in the previous tile's pass 1)
+        // (s_tile[par ^ 1] was last read by the previous tile's selection)
+        if (tid == 0) {
+            uint32_t st = s_state;
+            if (from_tma) st ^= 2u << par;  // this buffer's phase completed
+            if (t + (int)gridDim.x < n_tiles()) {
+                const Tile Tn = tile_of(t + gridDim.x);
+                publish(Tn, par ^ 1u);
+                if (Tn.inside && kp.tma_in) issue_load(Tn, par ^ 1u);
+            }
+            s_state = st ^ 1u;  // read again only after the tile's last barrier
         }
-    }
+        if constexpr (C::SEG) {
+            // parity layout: element e of parity row (par, ry) = columns c, c+1,
+            // c = 2 (e - PADE) + par; arrays A-even, A-odd, B-even, B-odd
+            for (int idx = tid; idx < 2 * C::RECN2; idx += NT) {
+                const int par = idx >= C::RECN2 ? 1 : 0, k = idx - par * C::RECN2;
+                const int ry = k / C::RWS2, e = k - ry * C::RWS2;
+                const int r0 = 2 * (e - C::PADE) + par, r1 = r0 + 1;
+                const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
+                const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
+                sA[idx] = make_float4(f.x, s.x, f.y, s.y);
+                sA[2 * C::RECN2 + idx] = make_float4(f.z, s.z, f.w, s.w);
+            }
+        } else {
+            for (int idx = tid; idx < C::RECN; idx += NT) {
+                const int ry = idx / RWS, c = idx - ry * RWS;
+                const int r0 = c - PADC, r1 = r0 + 1;
+                const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
+                const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
+                sA[idx] = make_float4(f.x, s.x, f.y, s.y);
+                sB[idx] = make_float4(f.z, s.z, f.w, s.w);
+            }
+        }
+        __syncthreads();
 
-    if constexpr (C::SEG) {
-        seg_stages<S, FAM, ST, PC, OPT, TR>(sA, sD, zchk, kp, ag, cen, aA, aL);
-    } else
-    static_for<0, S / C::G>([&](auto g_c) {
-        constexpr int g0 = decltype(g_c)::value * C::G;
-        constexpr int total = C::item_off(g0 + C::G - 1) + (RH - (g0 + C::G - 1)) * RW;
-        // ---- stage 1: pair distances of the region, each pair once --------
-        // thread item = pixel p (scalars in registers) for one row offset du;
-        // partners q, q+1 per packed step at constant offsets in padded rows;
-        // the items of the group's row offsets are flattened for balance
-        auto stage1 = [&](auto zc_c) {
-            constexpr bool ZC = decltype(zc_c)::value;
-            for (int itg = tid; itg < total; itg += NT) {
-                static_for<g0, g0 + C::G>([&](auto du_c) {
-                    constexpr int du = decltype(du_c)::value;
-                    constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
-                    constexpr int ndv = C::ndv_of(du);
-                    constexpr int NK2 = (ndv + 1) / 2;
-                    constexpr int i0 = C::item_off(du), cnt = (RH - du) * RW;
-                    constexpr int pl = C::plane_off(du);
-                    if (C::G == 1 || (itg >= i0 && itg < i0 + cnt)) {
-                        const int it = itg - i0;
-                        const int py = it / RW, px = it - py * RW;
-                        const int pidx = py * RWS + PADC + px;
-                        const float4 a4 = lds_f4(sA + pidx), b4 = lds_f4(sB + pidx);
-                        const Pix p = {a4.x, a4.z, b4.x, b4.z};
-                        const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
-                        const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
-    #pragma unroll
-                        for (int kk = 0; kk < NK2; kk++) {
-                            const ulonglong2 A2 = lds_u2(qa + 2 * kk), B2 = lds_u2(qb + 2 * kk);
-                            const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
-                            P2 da, dl;
-                            pair_values2<FAM, ST, PC, ZC>(p, q, kp, da, dl);
-                            const int k0 = pl + 2 * kk;
-                            const bool second = 2 * kk + 1 < ndv;
-                            if constexpr (BOTH) {
-                                sD[k0 * RN + it] = make_float2(lo2(da), lo2(dl));
-                                if (second) sD[(k0 + 1) * RN + it] = make_float2(hi2(da), hi2(dl));
-                            } else if constexpr (C::NEED_A) {
-                                sD[k0 * RN + it] = lo2(da);
-                                if (second) sD[(k0 + 1) * RN + it] = hi2(da);
-                            } else {
-                                sD[k0 * RN + it] = lo2(dl);
-                                if (second) sD[(k0 + 1) * RN + it] = hi2(dl);
+        // aggregates: BOTH -> packed (angular, Minkowski) pairs; else scalars
+        P2 ag[OPT][BOTH ? N : 1];
+        DT cen[OPT][CEN ? N : 1];  // centre column (angular, Minkowski) or (Minkowski)
+        float aA[OPT][(C::NEED_A && !BOTH) ? N : 1], aL[OPT][(C::NEED_L && !BOTH) ? N : 1];
+#pragma unroll
+        for (int o = 0; o < OPT; o++) {
+#pragma unroll
+            for (int i = 0; i < N; i++) {
+                if constexpr (BOTH) ag[o][i] = pk2(kp.self_term, 0.f);
+                else if constexpr (C::NEED_A) aA[o][i] = kp.self_term;
+                else aL[o][i] = 0.f;
+            }
+            if constexpr (CEN) {
+                if constexpr (BOTH) cen[o][DC] = make_float2(kp.self_term, 0.f);
+                else cen[o][DC] = dt_zero(DT());
+            }
+        }
+
+        if constexpr (C::SEG) {
+            seg_stages<S, FAM, ST, PC, OPT, TR>(sA, sD, zchk, kp, ag, cen, aA, aL, tid);
+        } else
+        static_for<0, S / C::G>([&](auto g_c) {
+            constexpr int g0 = decltype(g_c)::value * C::G;
+            constexpr int total = C::item_off(g0 + C::G - 1) + (RH - (g0 + C::G - 1)) * RW;
+            // ---- stage 1: pair distances of the region, each pair once --------
+            // thread item = pixel p (scalars in registers) for one row offset du;
+            // partners q, q+1 per packed step at constant offsets in padded rows;
+            // the items of the group's row offsets are flattened for balance
+            auto stage1 = [&](auto zc_c) {
+                constexpr bool ZC = decltype(zc_c)::value;
+                for (int itg = tid; itg < total; itg += NT) {
+                    static_for<g0, g0 + C::G>([&](auto du_c) {
+                        constexpr int du = decltype(du_c)::value;
+                        constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
+                        constexpr int ndv = C::ndv_of(du);
+                        constexpr int NK2 = (ndv + 1) / 2;
+                        constexpr int i0 = C::item_off(du), cnt = (RH - du) * RW;
+                        constexpr int pl = C::plane_off(du);
+                        if (C::G == 1 || (itg >= i0 && itg < i0 + cnt)) {
+                            const int it = itg - i0;
+                            const int py = it / RW, px = it - py * RW;
+                            const int pidx = py * RWS + PADC + px;
+                            const float4 a4 = lds_f4(sA + pidx), b4 = lds_f4(sB + pidx);
+                            const Pix p = {a4.x, a4.z, b4.x, b4.z};
+                            const ulonglong2 *qa = reinterpret_cast<const ulonglong2 *>(sA + pidx + du * RWS + dv0);
+                            const ulonglong2 *qb = reinterpret_cast<const ulonglong2 *>(sB + pidx + du * RWS + dv0);
+        #pragma unroll
+                            for (int kk = 0; kk < NK2; kk++) {
+                                const ulonglong2 A2 = lds_u2(qa + 2 * kk), B2 = lds_u2(qb + 2 * kk);
+                                const Pair2 q = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
+                                P2 da, dl;
+                                pair_values2<FAM, ST, PC, ZC>(p, q, kp, da, dl);
+                                const int k0 = pl + 2 * kk;
+                                const bool second = 2 * kk + 1 < ndv;
+                                if constexpr (BOTH) {
+                                    sD[k0 * RN + it] = make_float2(lo2(da), lo2(dl));
+                                    if (second) sD[(k0 + 1) * RN + it] = make_float2(hi2(da), hi2(dl));
+                                } else if constexpr (C::NEED_A) {
+                                    sD[k0 * RN + it] = lo2(da);
+                                    if (second) sD[(k0 + 1) * RN + it] = hi2(da);
+                                } else {
+                                    sD[k0 * RN + it] = lo2(dl);
+                                    if (second) sD[(k0 + 1) * RN + it] = hi2(dl);
+                                }
+                            }
+                        }
+                    });
+                }
+            };
+            if (zchk) stage1(std::true_type{});
+            else stage1(std::false_type{});
+            __syncthreads();
+            // ---- stage 2: window aggregation from the planes ------------------
+            // rows r = 0 .. S-du-1+OPT-1 below the thread's first output row feed
+            // output o's window row u = r - o.
+            const DT *dbase = sD + (ty * OPT) * RW + tx;
+            static_for<g0, g0 + C::G>([&](auto du_c) {
+                constexpr int du = decltype(du_c)::value;
+                constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
+                constexpr int ndv = C::ndv_of(du);
+                constexpr int pl = C::plane_off(du);
+                static_for<0, ndv>([&](auto k_c) {
+                    constexpr int k = decltype(k_c)::value;
+                    constexpr int dv = dv0 + k;
+                    constexpr int vlo = dv < 0 ? -dv : 0, vhi = dv > 0 ? S - dv : S;
+#pragma unroll
+                    for (int r = 0; r < S - du + OPT - 1; r++) {
+#pragma unroll
+                        for (int v = vlo; v < vhi; v++) {
+                            const DT val = dbase[(pl + k) * RN + r * RW + v];
+#pragma unroll
+                            for (int o = 0; o < OPT; o++) {
+                                const int u = r - o;
+                                if (u < 0 || u + du >= S) continue;
+                                const int i = u * S + v, j = (u + du) * S + v + dv;
+                                if constexpr (BOTH) {
+                                    const P2 x = *reinterpret_cast<const P2 *>(&val);
+                                    ag[o][i] = add2(ag[o][i], x);
+                                    ag[o][j] = add2(ag[o][j], x);
+                                } else if constexpr (C::NEED_A) {
+                                    aA[o][i] += val;
+                                    aA[o][j] += val;
+                                } else {
+                                    aL[o][i] += val;
+                                    aL[o][j] += val;
+                                }
+                                if constexpr (CEN) {
+                                    if (j == DC) cen[o][i] = val;
+                                    else if (i == DC) cen[o][j] = val;
+                                }
                             }
                         }
                     }
                 });
-            }
-        };
-        if (zchk) stage1(std::true_type{});
-        else stage1(std::false_type{});
-        __syncthreads();
-        // ---- stage 2: window aggregation from the planes ------------------
-        // rows r = 0 .. S-du-1+OPT-1 below the thread's first output row feed
-        // output o's window row u = r - o.
-        const DT *dbase = sD + (ty * OPT) * RW + tx;
-        static_for<g0, g0 + C::G>([&](auto du_c) {
-            constexpr int du = decltype(du_c)::value;
-            constexpr int dv0 = (du == 0) ? 1 : -(S - 1);
-            constexpr int ndv = C::ndv_of(du);
-            constexpr int pl = C::plane_off(du);
-            static_for<0, ndv>([&](auto k_c) {
-                constexpr int k = decltype(k_c)::value;
-                constexpr int dv = dv0 + k;
-                constexpr int vlo = dv < 0 ? -dv : 0, vhi = dv > 0 ? S - dv : S;
-#pragma unroll
-                for (int r = 0; r < S - du + OPT - 1; r++) {
-#pragma unroll
-                    for (int v = vlo; v < vhi; v++) {
-                        const DT val = dbase[(pl + k) * RN + r * RW + v];
-#pragma unroll
-                        for (int o = 0; o < OPT; o++) {
-                            const int u = r - o;
-                            if (u < 0 || u + du >= S) continue;
-                            const int i = u * S + v, j = (u + du) * S + v + dv;
-                            if constexpr (BOTH) {
-                                const P2 x = *reinterpret_cast<const P2 *>(&val);
-                                ag[o][i] = add2(ag[o][i], x);
-                                ag[o][j] = add2(ag[o][j], x);
-                            } else if constexpr (C::NEED_A) {
-                                aA[o][i] += val;
-                                aA[o][j] += val;
-                            } else {
-                                aL[o][i] += val;
-                                aL[o][j] += val;
-                            }
-                            if constexpr (CEN) {
-                                if (j == DC) cen[o][i] = val;
-                                else if (i == DC) cen[o][j] = val;
-                            }
-                        }
-                    }
-                }
             });
+            __syncthreads();
         });
-        __syncthreads();
-    });
 
-    // ---- stage 3: selection ------------------------------------------------
-    const int ox = tile_x0 + tx;
+
+        // ---- stage 3: selection -> the tile's output colours in sOut --------
+        // (tile coordinates re-read: not held live through the stages; the
+        // next tile publishes into the other parity slot)
+        const int tile_x0b = s_tile[par][0], tile_y0b = s_tile[par][1], frameb = s_tile[par][2];
+        uint8_t *sOut = sOut0 + par * C::kOutBuf;
+        const int ox = tile_x0b + tx;
 #pragma unroll
-    for (int o = 0; o < OPT; o++) {
-        const int ry0 = ty * OPT + o;  // window top row in region coordinates
-        const int oy = tile_y0 + ry0;
-        const bool valid = (oy < kp.out_rows) && (ox < kp.W);
+        for (int o = 0; o < OPT; o++) {
+            const int ry0 = ty * OPT + o;  // window top row in region coordinates
+            const int oy = tile_y0b + ry0;
+            const bool valid = (oy < kp.out_rows) && (ox < kp.W);
         uint32_t kc;
-        bool doubt;
-        {
-            // window colours: up to 5x5 loaded once into registers for the
-            // selection's passes (every pick reads each candidate's colour
-            // twice); 7x7 reads them from shared memory (49 more registers
-            // would spill the aggregates)
-            constexpr bool WCR = N <= 25;
-            uint32_t wc[WCR ? N : 1];
-            if constexpr (WCR) {
+            bool doubt;
+            {
+                // window colours: up to 5x5 loaded once into registers for the
+                // selection's passes (every pick reads each candidate's colour
+                // twice); 7x7 reads them from shared memory (49 more registers
+                // would spill the aggregates)
+                constexpr bool WCR = N <= 25;
+                uint32_t wc[WCR ? N : 1];
+                if constexpr (WCR) {
 #pragma unroll
-                for (int i = 0; i < N; i++) wc[i] = sK[(ry0 + i / S) * RW + tx + i % S];
+                    for (int i = 0; i < N; i++) wc[i] = sK[(ry0 + i / S) * RW + tx + i % S];
+                }
+                auto col = [&](auto ic) {
+                    constexpr int i = decltype(ic)::value;
+                    if constexpr (WCR) return wc[i];
+                    else return sK[(ry0 + i / S) * RW + tx + i % S];
+                };
+                if constexpr (BOTH) {
+                    auto A = [&](auto ic) { return lo2(ag[o][decltype(ic)::value]); };
+                    auto L = [&](auto ic) { return hi2(ag[o][decltype(ic)::value]); };
+                    auto AD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value].x; else return 0.f; };
+                    auto LD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value].y; else return 0.f; };
+                    select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, kc, doubt);
+                } else if constexpr (C::NEED_A) {
+                    auto V = [&](auto ic) { return aA[o][decltype(ic)::value]; };
+                    auto Z = [](auto) { return 0.f; };
+                    select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, kc, doubt);
+                } else {
+                    auto V = [&](auto ic) { return aL[o][decltype(ic)::value]; };
+                    auto Z = [](auto) { return 0.f; };
+                    auto CD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value]; else return 0.f; };
+                    select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, col, kc, doubt);
+                }
             }
-            auto col = [&](auto ic) {
-                constexpr int i = decltype(ic)::value;
-                if constexpr (WCR) return wc[i];
-                else return sK[(ry0 + i / S) * RW + tx + i % S];
-            };
-            if constexpr (BOTH) {
-                auto A = [&](auto ic) { return lo2(ag[o][decltype(ic)::value]); };
-                auto L = [&](auto ic) { return hi2(ag[o][decltype(ic)::value]); };
-                auto AD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value].x; else return 0.f; };
-                auto LD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value].y; else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, col, kc, doubt);
-            } else if constexpr (C::NEED_A) {
-                auto V = [&](auto ic) { return aA[o][decltype(ic)::value]; };
-                auto Z = [](auto) { return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, Z, col, kc, doubt);
-            } else {
-                auto V = [&](auto ic) { return aL[o][decltype(ic)::value]; };
-                auto Z = [](auto) { return 0.f; };
-                auto CD = [&](auto ic) { if constexpr (CEN) return cen[o][decltype(ic)::value]; else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, col, kc, doubt);
-            }
-        }
 
         if (kp.dbg != nullptr && valid) {
-            float *d = kp.dbg + ((long long)frame * kp.out_rows * kp.W + (long long)oy * kp.W + ox) * (2 * N);
+                float *d = kp.dbg + ((long long)frameb * kp.out_rows * kp.W + (long long)oy * kp.W + ox) * (2 * N);
 #pragma unroll
-            for (int i = 0; i < N; i++) {
-                if constexpr (BOTH) {
-                    d[i] = lo2(ag[o][i]);
-                    d[N + i] = hi2(ag[o][i]);
-                } else {
-                    d[i] = C::NEED_A ? aA[o][i] : 0.f;
-                    d[N + i] = C::NEED_L ? aL[o][i] : 0.f;
+                for (int i = 0; i < N; i++) {
+                    if constexpr (BOTH) {
+                        d[i] = lo2(ag[o][i]);
+                        d[N + i] = hi2(ag[o][i]);
+                    } else {
+                        d[i] = C::NEED_A ? aA[o][i] : 0.f;
+                        d[N + i] = C::NEED_L ? aL[o][i] : 0.f;
+                    }
                 }
             }
-        }
 
-        if (valid) {
-            const uint32_t col = kc;
-            uint8_t *op = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch + ox * 3;
-            op[0] = (uint8_t)(col & 0xff);
-            op[1] = (uint8_t)((col >> 8) & 0xff);
-            op[2] = (uint8_t)((col >> 16) & 0xff);
-        }
-        if (valid && doubt && !kp.diag_no_fixup) {
-            const unsigned slot = atomicAdd(&s_nflag, 1u);
-            s_flag[slot] = (uint16_t)((ry0 << 5) | tx);
-        }
-    }
-
-    // ---- stage 4: float64 re-decision of this CTA's doubtful pixels ---------
-    // All threads of the CTA evaluate the window's pair table (the planes'
-    // shared memory is free now), one warp aggregates and selects; the
-    // work overlaps with other CTAs' FP32 stages on the same SM.
-    __syncthreads();
-    const unsigned nflag = s_nflag;
-    if (nflag == 0) return;
-    if (tid == 0) atomicAdd(kp.flag_count, nflag);
-    constexpr int P = N * (N - 1) / 2;
-    static_assert(N * sizeof(E64) + 2 * P * sizeof(double) <= C::NPL * C::RN * sizeof(DT),
-                  "float64 scratch must fit in the plane buffer");
-    E64 *e64 = reinterpret_cast<E64 *>(sD);
-    double *dA = reinterpret_cast<double *>(e64 + N);
-    double *dL = dA + P;
-    const FParams &fp = kp.fp;
-    for (unsigned f = 0; f < nflag; f++) {
-        const int code = s_flag[f];
-        const int ry0 = code >> 5, cx = code & 31;
-        for (int i = tid; i < N; i += NT) {
-            const uint32_t col = sK[(ry0 + i / S) * RW + cx + i % S];
-            prep64(make_float4((float)(col & 0xff), (float)((col >> 8) & 0xff), (float)((col >> 16) & 0xff), 0.f),
-                   ST, e64[i]);
-        }
-        __syncthreads();
-        pair_tables<false>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
-        __syncthreads();
-        if (ty == 0) {
-            bool close;
-            const int bb = decide64<N, FAM, ST>(e64, fp, tx, dA, dL, &close);
-            if (tx == 0) { s_b = bb; s_close = close; }
-        }
-        __syncthreads();
-        if (ST == ST_EXACT && C::NEED_A && s_close) {
-            // pass 2: correctly rounded arccos (dfg_f64.cuh)
-            if (tid == 0) atomicAdd(kp.flag_count + 1, 1u);
-            pair_tables<true>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
-            __syncthreads();
-            if (ty == 0) {
-                bool close;
-                const int bb = decide64<N, FAM, ST>(e64, fp, tx, dA, dL, &close);
-                if (tx == 0) s_b = bb;
+            {
+                uint8_t *op = sOut + ry0 * 96 + 3 * tx;
+                op[0] = (uint8_t)(kc & 0xff);
+                op[1] = (uint8_t)((kc >> 8) & 0xff);
+                op[2] = (uint8_t)((kc >> 16) & 0xff);
             }
-            __syncthreads();
+            if (valid && doubt && !kp.diag_no_fixup) {
+                const unsigned slot = atomicAdd(&s_nflag, 1u);
+                s_flag[slot] = (uint16_t)((ry0 << 5) | tx);
+            }
         }
-        if (tid == 0) {
-            const int bb = s_b;
-            const uint32_t col = sK[(ry0 + bb / S) * RW + cx + bb % S];
-            uint8_t *op = out + (long long)frame * kp.out_fstride + (long long)(tile_y0 + ry0) * kp.out_pitch +
-                          (tile_x0 + cx) * 3;
-            op[0] = (uint8_t)(col & 0xff);
-            op[1] = (uint8_t)((col >> 8) & 0xff);
-            op[2] = (uint8_t)((col >> 16) & 0xff);
-        }
+
+        // ---- stage 4: float64 re-decision of this tile's doubtful pixels ----
+        // All threads evaluate the window's pair table (the planes' shared
+        // memory is free now), one warp aggregates and selects; the result
+        // replaces the pixel's colour in sOut.
         __syncthreads();
+        const unsigned nflag = s_nflag;
+        if (nflag != 0) {
+            if (tid == 0) atomicAdd(kp.flag_count, nflag);
+            constexpr int P = N * (N - 1) / 2;
+            static_assert(N * sizeof(E64) + 2 * P * sizeof(double) <= C::NPL * C::RN * sizeof(DT),
+                          "float64 scratch must fit in the plane buffer");
+            E64 *e64 = reinterpret_cast<E64 *>(sD);
+            double *dA = reinterpret_cast<double *>(e64 + N);
+            double *dL = dA + P;
+            const FParams &fp = kp.fp;
+            for (unsigned f = 0; f < nflag; f++) {
+                const int code = s_flag[f];
+                const int ry0 = code >> 5, cx = code & 31;
+                for (int i = tid; i < N; i += NT) {
+                    const uint32_t col = sK[(ry0 + i / S) * RW + cx + i % S];
+                    prep64(make_float4((float)(col & 0xff), (float)((col >> 8) & 0xff), (float)((col >> 16) & 0xff),
+                                       0.f),
+                           ST, e64[i]);
+                }
+                __syncthreads();
+                pair_tables<false>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
+                __syncthreads();
+                if (ty == 0) {
+                    bool close;
+                    const int bb = decide64<N, FAM, ST>(e64, fp, tx, dA, dL, &close);
+                    if (tx == 0) { s_b = bb; s_close = close; }
+                }
+                __syncthreads();
+                if (ST == ST_EXACT && C::NEED_A && s_close) {
+                    // pass 2: correctly rounded arccos (dfg_f64.cuh)
+                    if (tid == 0) atomicAdd(kp.flag_count + 1, 1u);
+                    pair_tables<true>(e64, fp, tid, NT, dA, dL, C::NEED_A, C::NEED_L);
+                    __syncthreads();
+                    if (ty == 0) {
+                        bool close;
+                        const int bb = decide64<N, FAM, ST>(e64, fp, tx, dA, dL, &close);
+                        if (tx == 0) s_b = bb;
+                    }
+                    __syncthreads();
+                }
+                if (tid == 0) {
+                    const int bb = s_b;
+                    const uint32_t col = sK[(ry0 + bb / S) * RW + cx + bb % S];
+                    uint8_t *op = sOut + ry0 * 96 + 3 * cx;
+                    op[0] = (uint8_t)(col & 0xff);
+                    op[1] = (uint8_t)((col >> 8) & 0xff);
+                    op[2] = (uint8_t)((col >> 16) & 0xff);
+                }
+                __syncthreads();
+            }
+        }
+
+        // ---- the tile's colours -> global memory -----------------------------
+        // (bulk store: issued after the tile's last barrier; it overlaps the
+        // next tile and is waited for two tiles later)
+        if (kp.tma_out) {
+            fence_proxy_async();  // sOut writes visible to the bulk copy
+        } else {
+            __syncthreads();
+            for (int b = tid; b < TH * 96; b += NT) {
+                const int ry = b / 96, xb = b - ry * 96;
+                if (tile_y0b + ry < kp.out_rows && tile_x0b * 3 + xb < 3 * kp.W)
+                    out[(long long)frameb * kp.out_fstride + (long long)(tile_y0b + ry) * kp.out_pitch + 3 * tile_x0b + xb] =
+                        sOut[b];
+            }
+        }
+        __syncthreads();  // the next tile reuses every buffer
+        if (kp.tma_out && tid == 0) tma_store_3d(&kp.tm_out, 3 * tile_x0b, tile_y0b, frameb, sOut);
     }
+    if (threadIdx.x == 0 && kp.tma_out) tma_store_wait_all();
 }
 
 // Per (window, family) launch shape: OPT outputs per thread (register
@@ -1358,7 +1609,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
 template <int FAM, int ST, int PC>
 cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp);  // dfg_w3.cuh
 
-template <int S, int FAM>
+template <int S, int FAM, int ST>
 struct Shape {
     static constexpr int AGG =
         ((FamT<FAM>::A ? 1 : 0) + (FamT<FAM>::L ? 1 : 0)) * (FamT<FAM>::CEN ? 2 : 1) * S * S;
@@ -1368,11 +1619,17 @@ struct Shape {
     // so the bound is warps per sub-partition, not per SM.
     static constexpr int WPS = 16384 / (REG * 32);
     static constexpr int TR0 = WPS >= 4 ? 8 : 4 * (WPS < 2 ? 2 : WPS);
-    static constexpr int TR = (S == 3 && !FamT<FAM>::CEN) ? 16 : TR0;  // 16 warps x 2 CTAs, 64 registers
     static constexpr int MINB0 = WPS >= 4 ? (WPS / 2 > 4 ? 4 : WPS / 2) : 1;
-    // 3x3 BVDF/DDF/VMF: 4 CTAs (32 warps) per SM hide the staging and
-    // barrier latency better than the few extra registers would
-    static constexpr int MINB = (S == 3 && !FamT<FAM>::CEN) ? 2 : MINB0;
+    // 5x5 / 7x7 minimax shapes that would run two CTAs per SM run one CTA
+    // of twice the warps instead: a taller tile (less halo re-evaluation:
+    // C4 DDF 432 -> 720 region pixels for 256 -> 512 outputs), the same
+    // warps per SM, no register spills at 128 (measured: ddf:minimax 4.53 ->
+    // 3.63 ms, bvdf:minimax 2.59 -> 2.30; the chromaticity route, lighter
+    // per pair, keeps two CTAs with pixel-pair items: 1.35 vs 1.89 ms);
+    // 3x3 BVDF/DDF/VMF: 2 CTAs of 16 warps at 64 registers
+    static constexpr bool WIDE = S >= 5 && MINB0 >= 2 && ST == ST_MINIMAX;
+    static constexpr int TR = (S == 3 && !FamT<FAM>::CEN) ? 16 : (WIDE ? 2 * TR0 : TR0);
+    static constexpr int MINB = (S == 3 && !FamT<FAM>::CEN) ? 2 : (WIDE ? MINB0 / 2 : MINB0);
 };
 
 template <int S, int FAM, int ST, int PC>
@@ -1390,19 +1647,32 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
                         (force ? force == 1 : (kp.w3_rpc > 0 || strip_rows >= 8192));
         if (w3) return launch_w3<FAM, ST, PC>(st, in, out, kp);
     }
-    using SH = Shape<S, FAM>;
+    using SH = Shape<S, FAM, ST>;
     using C = Cfg<S, FAM, SH::OPT, SH::TR>;
     auto kern = dfg_fast_kernel<S, FAM, ST, PC, SH::OPT, SH::TR, SH::MINB>;
-    static unsigned long long configured = 0;  // per-device bit, idempotent
+    static int resident[64] = {};  // CTAs per SM, per device
     int dev = 0;
     cudaGetDevice(&dev);
-    if (!(configured & (1ull << (dev & 63)))) {
+    if (resident[dev & 63] == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::kSmem);
         if (e != cudaSuccess) return e;
-        configured |= 1ull << (dev & 63);
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, C::NT, C::kSmem);
+        if (e != cudaSuccess) return e;
+        resident[dev & 63] = nb > 0 ? nb : 1;
     }
-    dim3 grid((kp.W + 31) / 32, (kp.out_rows + C::TH - 1) / C::TH, kp.n_frames);
-    kern<<<grid, C::NT, C::kSmem, st>>>(in, out, kp);
+    KParams k2 = kp;
+    // bulk tensor maps over the input / output rows (uint8, 3W bytes wide)
+    const int box_in[3] = {C::kRawPitch, C::RH, 1}, box_out[3] = {96, C::TH, 1};
+    k2.tma_in = (options().tma & 1) && encode_rows_map(&k2.tm_in, in, 3LL * kp.W, kp.in_rows, kp.n_frames, kp.in_pitch,
+                                                 kp.in_fstride, box_in);
+    k2.tma_out = (options().tma & 2) && encode_rows_map(&k2.tm_out, out, 3LL * kp.W, kp.out_rows, kp.n_frames,
+                                                  kp.out_pitch, kp.out_fstride, box_out);
+    // persistent CTAs: one wave, each walking tiles
+    const long long tiles = (long long)((kp.W + 31) / 32) * ((kp.out_rows + C::TH - 1) / C::TH) * kp.n_frames;
+    const long long slots = (long long)sm_count(dev) * resident[dev & 63];
+    const int grid = (int)(tiles < slots || !options().persist ? tiles : slots);
+    kern<<<grid, C::NT, C::kSmem, st>>>(in, out, k2);
     return cudaGetLastError();
 }
 

@@ -2,6 +2,7 @@
 // filter kernels (fast FP32 decision kernel + float64 re-decision kernel).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -33,8 +34,14 @@ struct FParams {
     double cr_margin;  // relative decision margin below which pass 2 (CR acos) runs
 };
 
-// Kernel-side parameter block, passed by value.
+// Kernel-side parameter block, passed by value (__grid_constant__: the
+// tensor maps are read in place).
 struct KParams {
+    // bulk tensor maps of the input rows and the output rows ((3W bytes) x
+    // rows x frames, uint8), valid when tma_in / tma_out (host-checked
+    // alignment); the 5x5 / 7x7 / 3x3-CTA kernel uses them
+    CUtensorMap tm_in, tm_out;
+    int tma_in, tma_out;
     // geometry (rows are global image rows; see dfg_filter_rows)
     int global_H, W;
     int in_row0, in_rows;
@@ -80,9 +87,16 @@ struct Options {
     int w3_rpc = 0;         // DFG_OPT_W3_RPC: rows per chunk of the 3x3 row sweep (0 auto)
     int w3_small_wps = 12;  // DFG_OPT_W3_SMALL_WPS: warps per SM for single-wave 3x3 frames
     double cr_margin = 1e-12;  // DFG_OPT_CR_MARGIN: relative margin that triggers the CR-acos pass
+    int persist = 1;        // DFG_OPT_PERSIST: CTA kernels as one wave of persistent CTAs (0: one tile per CTA)
+    int tma = 3;            // DFG_OPT_TMA: bulk tensor copies of the CTA kernels' tiles: 1 input, 2 output, 3 both
 };
 Options &options();
 int sm_count(int dev);  // multiProcessorCount, cached per device
+// A 3-D uint8 tensor map (row bytes x rows x frames) with the given box;
+// false when the base / strides do not meet the bulk-copy alignment rules
+// (16-byte base and strides) or the driver entry point is unavailable.
+bool encode_rows_map(CUtensorMap *map, const void *base, long long row_bytes, int rows, int frames, long long pitch,
+                     long long fstride, const int box[3]);
 
 // Border policy resolution (image.py:158-176): replicate = clamp,
 // reflect = numpy 'symmetric' (edge-inclusive mirror, periodic).

@@ -11,9 +11,9 @@ tag, launches, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
 out = [f"# ncu summaries, round {tag}", "",
        "Captured on one B200 (sm_100a, driver 580.159) through `gpurun` with "
        "`ncu --set full --clock-control none --import-source on -k 'regex:dfg_w3_kernel|dfg_fast_kernel' -s 3 -c 1` on "
-       "`python bench.py --config <c> --steps 1 --warmup 3 --no-cpu` (the 4th launch: after the 3 warm-up steps), "
+       "`python bench.py --config <c> --steps 1 --warmup 3 --no-cpu --no-parity --no-table` (the 4th launch: after the 3 warm-up steps), "
        "and the launch list with `--metrics gpu__time_duration.sum,... --clock-control none -c 400` on the default "
-       "bench command (`scripts/gpu_final.sh`). "
+       "bench command (`scripts/gpu_profiles.sh`). "
        "Durations under ncu are cold-cache and serialised; the bench numbers come from CUDA events without ncu.", ""]
 
 # launch list shares
@@ -24,7 +24,7 @@ agg = collections.defaultdict(lambda: collections.defaultdict(list))
 for r in rows[1:]:
     agg[r[ki]][r[mi]].append(float(r[vi].replace(",", "")))
 tot = sum(sum(m["gpu__time_duration.sum"]) for m in agg.values())
-out += ["## Launch list of the default bench command (C2: ddf:exact, 1024x1024)", "",
+out += ["## Launch list of the default bench command (C5a: ddf:exact:window=7, 8192x8192)", "",
         "| kernel | launches | mean time (us) | share of GPU time | warp instructions | registers | DRAM read+write per launch |",
         "|---|---|---|---|---|---|---|"]
 for k, m in sorted(agg.items(), key=lambda kv: -sum(kv[1]["gpu__time_duration.sum"])):

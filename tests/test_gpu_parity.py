@@ -334,3 +334,27 @@ def _raw_image(a):
     class _Img:
         pixels = a
     return _Img()
+
+
+@pytest.mark.parametrize("tma", [0, 1, 2, 3])
+@pytest.mark.parametrize("spec", ["ddf:exact:window=7", "acwddf:minimax:window=5", "bvdf:rgb:window=5", "vmf:window=7"])
+def test_tile_bulk_copies_on_and_off(cuda, spec, tma):
+    """The CTA kernel's bulk tensor copies (DFG_OPT_TMA bit 0: each
+    interior tile's region by TMA, prefetched a tile ahead; bit 1: the
+    tile's colours out by a TMA store) give the same pixels as indexed
+    loads / byte stores: 16-byte aligned rows (where the tensor maps apply),
+    a 3-frame batch (3-D maps) and a strip at an interior row offset."""
+    torch = cuda
+    s = parse_filter_spec(spec)
+    img = synth.noisy_image(160, 512, 13, ("correlated", 0.2))
+    frames = np.stack([synth.noisy_image(70, 256, 50 + i, ("uncorrelated", 0.15)) for i in range(3)])
+    with _lib.option("tma", tma):
+        got = filter_device(torch.from_numpy(img).cuda(), s).cpu().numpy()
+        gotb = filter_batch_device(torch.from_numpy(frames).cuda(), s).cpu().numpy()
+        x = torch.from_numpy(img).cuda()
+        gots = filter_rows_device(x[16:150], 160, 16, 40, 96, s).cpu().numpy()
+    want = oracle.filter_image(img, s)
+    assert (got == want).all(), (spec, tma, int((got != want).any(-1).sum()))
+    for i in range(3):
+        assert (gotb[i] == oracle.filter_image(frames[i], s)).all(), (spec, tma, i)
+    assert (gots == want[40:136]).all(), (spec, tma)
