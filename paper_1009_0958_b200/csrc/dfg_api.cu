@@ -106,8 +106,8 @@ int validate(const dfg_params *p)
         const int n = p->window * p->window, d = (n + 1) / 2;
         if (p->lam < 1 || p->lam > d) return fail(DFG_E_ARG, "smoothing level k must be in [1, (n+1)/2]");
     }
-    if (p->family != DFG_IDENTITY && p->window != 3 && p->window != 5 && p->window != 7)
-        return fail(DFG_E_UNSUP, "this build supports window sides 3, 5 and 7");
+    if (p->family != DFG_IDENTITY && p->window > dfg::kWideMaxSide)
+        return fail(DFG_E_UNSUP, "this build supports odd window sides 3 .. 31");
     return DFG_OK;
 }
 
@@ -169,6 +169,7 @@ cudaError_t launch_fast(const dfg_params *p, cudaStream_t st, const uint8_t *in,
                         const dfg::KParams &kp)
 {
     const int pc = pcode_of(p->p);
+    if (p->window > 7) return dfg::launch_wide(st, in, out, kp);  // float64 direct (dfg_wide.cu)
 #define DFG_CASE(S)                                                                    \
     if (p->window == S) {                                                              \
         switch (p->family) {                                                           \

@@ -489,7 +489,11 @@ struct Cfg {
     // the register budget allows their live set (>= 168 per thread: the
     // 1-CTA-per-SM shapes); one pixel per item otherwise
     static constexpr bool ITEM2 = NT * 168 <= 65536;
-    static constexpr int RECN2 = RH * RWS2;  // elements per parity array
+    // elements per parity array.  One-pixel items read both parities in one
+    // warp instruction (even lanes the even array, odd lanes the odd one):
+    // the arrays then sit 64 bytes apart modulo 128 (RECN2 = 4 mod 8), so the
+    // two lane groups of a 16-byte access use different banks
+    static constexpr int RECN2 = ITEM2 ? RH * RWS2 : ((RH * RWS2 + 3) & ~7) + 4;
     static constexpr size_t kRecBytes = SEG ? (size_t)RECN2 * 64 : (size_t)RECN * 32;
     // TMA buffers (128-byte aligned): two raw uint8 regions (box of 144 bytes
     // x RH rows: a tile load must start at a 16-byte aligned column, so the
@@ -826,12 +830,47 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
         else return hi ? hi2(dl) : lo2(dl);
     };
 
+    // ---- per-output accumulation of the segment sums of du: S_+du
+    // (u + du < S) and S_-du (u >= du; du = 0: the row's both-sided sums);
+    // one window row u per call ------------------------------------------
+    auto accumulate_row = [&](auto du_c, auto u_c) {
+        constexpr int du = decltype(du_c)::value, u = decltype(u_c)::value;
+        const DT *sPd = (du & 1) ? sP1 : sP0;
+        if constexpr (du == 0 || u + du < S || u >= du) {
+#pragma unroll
+            for (int o = 0; o < OPT; o++) {
+                const int ry0 = ty * OPT + o;
+#pragma unroll
+                for (int v = 0; v < S; v++) {
+                    const int i = u * S + v;
+                    const int qi = (ry0 + u) * RW + tx + v;
+                    DT add;
+                    if constexpr (du == 0) add = sM[v * RN + qi];
+                    else if constexpr (u + du < S && u >= du) add = dt_add(sPd[v * RN + qi], sM[v * RN + qi]);
+                    else if constexpr (u + du < S) add = sPd[v * RN + qi];
+                    else add = sM[v * RN + qi];
+                    if constexpr (BOTH) {
+                        ag[o][i] = add2(ag[o][i], *reinterpret_cast<const P2 *>(&add));
+                    } else if constexpr (C::NEED_A) {
+                        aA[o][i] += add;
+                    } else {
+                        aL[o][i] += add;
+                    }
+                }
+            }
+        }
+    };
+    auto accumulate = [&](auto du_c) { static_for<0, S>([&](auto u_c) { accumulate_row(du_c, u_c); }); };
+
     // ---- stage 1 of row offset du: planes (+ downward segment sums) --------
     auto stage1 = [&](auto du_c, auto zc_c) {
         constexpr int du = decltype(du_c)::value;
         constexpr bool ZC = decltype(zc_c)::value;
         constexpr int items = (RH - du) * RW2;
-        for (int it2 = tid; it2 < items; it2 += NT) {
+        // one item; `has` predicates its stores (a lane without an item of its
+        // own evaluates a clamped one); chunk(c), c = 0 .. S-1, is called after
+        // the c-th element evaluation (the interleaved accumulation below)
+        auto item = [&](const int it2, const bool has, auto &&chunk) {
             const int py = it2 / RW2, j = it2 - py * RW2;
             const int it0 = py * RW + 2 * j;
             const int pe = py * RWS2 + PADE + j;  // the item's own element: pixels (2j, 2j+1)
@@ -865,8 +904,10 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
                     constexpr int m = decltype(m_c)::value;
                     eval(m_c);
                     // t = 2m-1 (m > H) and t = 2m are complete for both pixels
-                    if constexpr (m > H) st_pair(sD + (2 * m - 1) * RN + it0, T0[2 * m - 1], T1[2 * m - 1]);
-                    st_pair(sD + (2 * m) * RN + it0, T0[2 * m], T1[2 * m]);
+                    if (has) {
+                        if constexpr (m > H) st_pair(sD + (2 * m - 1) * RN + it0, T0[2 * m - 1], T1[2 * m - 1]);
+                        st_pair(sD + (2 * m) * RN + it0, T0[2 * m], T1[2 * m]);
+                    }
                     // prefix sums over t = S-1 .. : R[k] = sum of T[S-1 .. S-1+k]
                     static_for<0, S>([&](auto k_c) {
                         constexpr int k = decltype(k_c)::value, t = S - 1 + k;
@@ -880,16 +921,17 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
                             }
                         }
                     });
+                    chunk(std::integral_constant<int, m - H>{});
                 });
                 DT *sPd = (du & 1) ? sP1 : sP0;
-                st_pair(sPd + it0, R0[S - 1], R1[S - 1]);  // v = 0: the whole right part
+                if (has) st_pair(sPd + it0, R0[S - 1], R1[S - 1]);  // v = 0: the whole right part
                 static_for<0, H>([&](auto mm_c) {           // left half, descending t
                     constexpr int m = H - 1 - decltype(mm_c)::value;
                     eval(std::integral_constant<int, m>{});
                     // t = 2m+1 and t = 2m complete (t = 2m+1 = S-2 first)
                     static_for<0, 2>([&](auto w_c) {
                         constexpr int t = 2 * m + 1 - decltype(w_c)::value;
-                        st_pair(sD + t * RN + it0, T0[t], T1[t]);
+                        if (has) st_pair(sD + t * RN + it0, T0[t], T1[t]);
                         if constexpr (t == S - 2) {
                             L0 = T0[t];
                             L1 = T1[t];
@@ -899,8 +941,9 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
                         }
                         // L = L[t]: segment sum of the window in which the
                         // pixel sits at column v = S-1-t
-                        st_pair(sPd + (S - 1 - t) * RN + it0, dt_add(L0, R0[t]), dt_add(L1, R1[t]));
+                        if (has) st_pair(sPd + (S - 1 - t) * RN + it0, dt_add(L0, R0[t]), dt_add(L1, R1[t]));
                     });
+                    chunk(std::integral_constant<int, H + 1 + decltype(mm_c)::value>{});
                 });
             } else {
                 // same row, partners to the right: odd-column elements
@@ -921,15 +964,16 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
                     pair_values2<FAM, ST, PC, ZC>(p1, q, kp, da1, dl1);
                     if constexpr (m > 0) {
                         T1[2 * m - 1] = to_dt(da1, dl1, false);
-                        st_pair(sD + (2 * m - 1) * RN + it0, T0[2 * m - 1], T1[2 * m - 1]);
+                        if (has) st_pair(sD + (2 * m - 1) * RN + it0, T0[2 * m - 1], T1[2 * m - 1]);
                     }
                     if constexpr (m < H) {
                         T1[2 * m] = to_dt(da1, dl1, true);
-                        st_pair(sD + (2 * m) * RN + it0, T0[2 * m], T1[2 * m]);
+                        if (has) st_pair(sD + (2 * m) * RN + it0, T0[2 * m], T1[2 * m]);
                     }
                 });
             }
-        }
+        };
+        for (int it2 = tid; it2 < items; it2 += NT) item(it2, true, [](auto) {});
     };
     // one-pixel items (register-tight shapes, Cfg::ITEM2 false): pixel p at
     // column c against the pair elements of c's parity, (q, q+1) at c - (S-1)
@@ -1033,50 +1077,16 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
         }
     };
 
-    // ---- per-output accumulation of the segment sums of du: S_+du
-    // (u + du < S) and S_-du (u >= du; du = 0: the row's both-sided sums) --
-    auto accumulate = [&](auto du_c) {
-        constexpr int du = decltype(du_c)::value;
-        const DT *sPd = (du & 1) ? sP1 : sP0;
-#pragma unroll
-        for (int o = 0; o < OPT; o++) {
-            const int ry0 = ty * OPT + o;
-#pragma unroll
-            for (int u = 0; u < S; u++) {
-#pragma unroll
-                for (int v = 0; v < S; v++) {
-                    const int i = u * S + v;
-                    const int qi = (ry0 + u) * RW + tx + v;
-                    DT add = dt_zero(DT());
-                    if (du == 0) {
-                        add = sM[v * RN + qi];
-                    } else if (u + du < S && u >= du) {
-                        add = dt_add(sPd[v * RN + qi], sM[v * RN + qi]);
-                    } else if (u + du < S) {
-                        add = sPd[v * RN + qi];
-                    } else if (u >= du) {
-                        add = sM[v * RN + qi];
-                    } else {
-                        continue;
-                    }
-                    if constexpr (BOTH) {
-                        ag[o][i] = add2(ag[o][i], *reinterpret_cast<const P2 *>(&add));
-                    } else if constexpr (C::NEED_A) {
-                        aA[o][i] += add;
-                    } else {
-                        aL[o][i] += add;
-                    }
-                }
-            }
-        }
-    };
-
     run_stage1(std::integral_constant<int, 0>{});
     __syncthreads();
     phase2(std::integral_constant<int, 0>{});
     __syncthreads();
     static_for<1, S>([&](auto du_c) {
         constexpr int du = decltype(du_c)::value;
+        // (interleaving this accumulation into the items, one window row per
+        // element evaluation, measured 4 % slower on C5a; running the two
+        // halves in opposite order on odd and even warps 63 % slower: two
+        // instruction streams thrash the instruction cache)
         run_stage1(du_c);
         accumulate(std::integral_constant<int, du - 1>{});
         __syncthreads();
@@ -1317,8 +1327,8 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                 const int par = idx >= C::RECN2 ? 1 : 0, k = idx - par * C::RECN2;
                 const int ry = k / C::RWS2, e = k - ry * C::RWS2;
                 const int r0 = 2 * (e - C::PADE) + par, r1 = r0 + 1;
-                const float4 f = (r0 >= 0 && r0 < RW) ? tmp[ry * RW + r0] : neutral;
-                const float4 s = (r1 >= 0 && r1 < RW) ? tmp[ry * RW + r1] : neutral;
+                const float4 f = (r0 >= 0 && r0 < RW && ry < RH) ? tmp[ry * RW + r0] : neutral;
+                const float4 s = (r1 >= 0 && r1 < RW && ry < RH) ? tmp[ry * RW + r1] : neutral;
                 sA[idx] = make_float4(f.x, s.x, f.y, s.y);
                 sA[2 * C::RECN2 + idx] = make_float4(f.z, s.z, f.w, s.w);
             }

@@ -91,6 +91,10 @@ struct Options {
     int tma = 3;            // DFG_OPT_TMA: bulk tensor copies of the CTA kernels' tiles: 1 input, 2 output, 3 both
 };
 Options &options();
+// Window sides above 7 run the float64 direct kernel (dfg_wide.cu), up to
+// this side (its per-CTA tables are n * 88 bytes of shared memory)
+constexpr int kWideMaxSide = 31;
+cudaError_t launch_wide(cudaStream_t st, const uint8_t *in, uint8_t *out, const struct KParams &kp);
 int sm_count(int dev);  // multiProcessorCount, cached per device
 // A 3-D uint8 tensor map (row bytes x rows x frames) with the given box;
 // false when the base / strides do not meet the bulk-copy alignment rules

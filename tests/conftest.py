@@ -23,6 +23,13 @@ def golden():
 
 
 @pytest.fixture(scope="session")
+def golden_wide():
+    """Window sides 9, 11, 13 run through the reference (tests/golden/make_golden_wide.py)."""
+    data = np.load(GOLDEN / "wide.npz")
+    return data, json.loads((GOLDEN / "wide_manifest.json").read_text())["cases"]
+
+
+@pytest.fixture(scope="session")
 def golden_full():
     """Same fixtures with the whole manifest (noise cases, metrics pairs)."""
     return np.load(GOLDEN / "filters.npz"), json.loads((GOLDEN / "manifest.json").read_text())

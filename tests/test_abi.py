@@ -70,7 +70,7 @@ def test_noise_and_metrics_validate_before_any_cuda_call():
                                None) == -1
 
 
-@pytest.mark.parametrize("text,code", [("vmf:window=9", _lib.DFG_E_UNSUP), ("bvdf:exact:window=11", _lib.DFG_E_UNSUP)])
+@pytest.mark.parametrize("text,code", [("vmf:window=33", _lib.DFG_E_UNSUP), ("bvdf:exact:window=101", _lib.DFG_E_UNSUP)])
 def test_unsupported_window_reported_before_any_cuda_call(text, code):
     L = _lib.lib()
     prm = _lib.params_from_spec(parse_filter_spec(text), "replicate")
