@@ -108,9 +108,14 @@ __device__ __forceinline__ void w3_redecide(const KParams &kp, const uint32_t *r
     }
 }
 
-// The row loop is unrolled by the ring period (3): in phase PH the current
-// row's ring slot is PH, the previous row's (PH + 2) % 3 and the one before
-// (PH + 1) % 3 -- compile-time slot addresses, no rotation moves.
+// The ring slots of rows y, y-1, y-2 rotate at run time.  (Measured in round
+// 2: unrolling the row loop by the ring period with compile-time slots --
+// no rotation moves, no slot arithmetic -- triples the step's code and ran
+// C2 45.7 -> 54.5 us, C5b 5.22 -> 7.53 ms: the instruction cache, not the
+// ~45 moves, is what the step is short of.  That experiment also showed why
+// the ring's record loads must be the ORDERED helper: with loop-invariant
+// addresses the compiler hoisted the plain (pure) asm loads above the
+// stores of the same step.)
 //
 // Aggregation by column sums (per window row t, for the lane's own pixel P_t
 // of that row): V_t(dv) = sum over the three window rows of d(P_t, (row,
@@ -257,8 +262,8 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
 #pragma unroll
             for (int t = 0; t < 5; t++) {
                 if (!need(t)) continue;
-                const ulonglong2 A2 = lds_u2(rA + rsl[t] * C::LANES_E + els[t] + lane);
-                const ulonglong2 B2 = lds_u2(rB + rsl[t] * C::LANES_E + els[t] + lane);
+                const ulonglong2 A2 = lds_u2_ordered(rA + rsl[t] * C::LANES_E + els[t] + lane);
+                const ulonglong2 B2 = lds_u2_ordered(rB + rsl[t] * C::LANES_E + els[t] + lane);
                 pp[t] = {{A2.x}, {A2.y}, {B2.x}, {B2.y}};
             }
             pp[5] = pv;
@@ -380,12 +385,17 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
                 auto L = [&](auto ic) { return hi2(ag[decltype(ic)::value]); };
                 auto AD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value].x; else return 0.f; };
                 auto LD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value].y; else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, colf, cb, doubt);
+                auto AL = [&](auto ic) { return ag[decltype(ic)::value]; };
+                auto CDP = [&](auto ic) {
+                    if constexpr (CEN) return *reinterpret_cast<const P2 *>(&cen[decltype(ic)::value]);
+                    else return P2{0ull};
+                };
+                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, colf, cb, doubt, AL, CDP);
             } else {
                 auto V = [&](auto ic) { return ag[decltype(ic)::value]; };
                 auto Z = [](auto) { return 0.f; };
                 auto CD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value]; else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, colf, cb, doubt);
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, colf, cb, doubt, Z, Z);
             }
         }
         uint8_t *orow = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch;

@@ -19,7 +19,7 @@ ST = {"exact": "ST_EXACT", "minimax": "ST_MINIMAX", "chroma": "ST_CHROMA"}
 body = "".join(
     f"    if (strategy == dfg::{ST[s]}) "
     f"return dfg::launch_fast<{S}, dfg::{FAM}, dfg::{ST[s]}, dfg::PC_2>(st, in, out, kp);\n" for s in strategies)
-src = f"""#include "dfg_fast.cuh"
+src = f"""#include "dfg_w3.cuh"
 cudaError_t dfg_launch_s{S}_{fam}(int strategy, int pcode, cudaStream_t st, const uint8_t *in, uint8_t *out,
                                   const dfg::KParams &kp)
 {{
