@@ -385,17 +385,12 @@ dfg_w3_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const _
                 auto L = [&](auto ic) { return hi2(ag[decltype(ic)::value]); };
                 auto AD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value].x; else return 0.f; };
                 auto LD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value].y; else return 0.f; };
-                auto AL = [&](auto ic) { return ag[decltype(ic)::value]; };
-                auto CDP = [&](auto ic) {
-                    if constexpr (CEN) return *reinterpret_cast<const P2 *>(&cen[decltype(ic)::value]);
-                    else return P2{0ull};
-                };
-                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, colf, cb, doubt, AL, CDP);
+                select_window<FAM, ST, N, DC>(kp, A, L, AD, LD, colf, cb, doubt);
             } else {
                 auto V = [&](auto ic) { return ag[decltype(ic)::value]; };
                 auto Z = [](auto) { return 0.f; };
                 auto CD = [&](auto ic) { if constexpr (CEN) return cen[decltype(ic)::value]; else return 0.f; };
-                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, colf, cb, doubt, Z, Z);
+                select_window<FAM, ST, N, DC>(kp, V, V, Z, CD, colf, cb, doubt);
             }
         }
         uint8_t *orow = out + (long long)frame * kp.out_fstride + (long long)oy * kp.out_pitch;
