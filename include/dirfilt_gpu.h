@@ -147,6 +147,14 @@ DFG_API int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *
 DFG_API int dfg_filter_host_f64(const double *h_in, int32_t H, int32_t W, double *h_out,
                     const dfg_params *prm, int32_t threads, void *stream);
 
+/* Test hook (CPU only): the float64 <-> uint8 conversions of
+ * dfg_filter_host_f64 (csrc/dfg_hostconv.cu).  Converts src[0..n) with the
+ * dispatched (AVX2) form into dst_fast and with the scalar form into dst_ref,
+ * and dst_ref back to float64 into `back`.  Returns bit 0 / bit 1: the
+ * dispatched / scalar form found a value that is not an integer in 0..255. */
+DFG_API int dfg_hostconv_selftest(const double *src, int64_t n, uint8_t *dst_fast, uint8_t *dst_ref,
+                    double *back);
+
 /* A stream of n independent (H, W, 3) frames from HOST memory (one buffer
  * per frame, pinned for overlap), synchronised before return: the
  * reference's per-frame apply_filter loop (bench.py:96-109, cli filter over

@@ -23,6 +23,7 @@ EXPORTS = (
     "dfg_set_option", "dfg_get_option", "dfg_fixup_count",
     "dfg_reset_counts", "dfg_debug_values", "dfg_cr_acos_host", "dfg_corrupt_image",
     "dfg_image_metrics", "dfg_calib_scratch_bytes", "dfg_calib_reduce", "dfg_calib_samples", "dfg_moments_reduce",
+    "dfg_hostconv_selftest",
 )
 
 
@@ -107,6 +108,8 @@ def lib() -> ctypes.CDLL:
     L.dfg_calib_reduce.argtypes = [ctypes.POINTER(DfgCalibParams), i32, ctypes.c_double, ctypes.c_double,
                                    ctypes.POINTER(ctypes.c_double), vp, sz, vp]
     L.dfg_calib_samples.argtypes = [ctypes.POINTER(DfgCalibParams), vp, vp, vp]
+    L.dfg_hostconv_selftest.argtypes = [vp, i64, vp, vp, vp]
+    L.dfg_hostconv_selftest.restype = ctypes.c_int
     L.dfg_moments_reduce.argtypes = [vp, vp, i64, i32, ctypes.c_double, ctypes.c_double,
                                      ctypes.POINTER(ctypes.c_double), vp, sz, vp]
     for name in ("dfg_filter", "dfg_filter_rows", "dfg_filter_batch", "dfg_filter_host", "dfg_filter_host_f64",

@@ -8,6 +8,9 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#if defined(__linux__)
+#include <sys/mman.h>
+#endif
 
 #include <atomic>
 #include <string>
@@ -17,6 +20,9 @@
 #include "dfg_internal.cuh"
 
 namespace dfg {
+
+unsigned f64_to_u8(const double *src, uint8_t *dst, size_t lo, size_t hi);  // dfg_hostconv.cu
+void u8_to_f64(const uint8_t *src, double *dst, size_t lo, size_t hi);
 
 Options &options()
 {
@@ -270,6 +276,7 @@ struct HostCache {
     cudaStream_t s_in = nullptr, s_out = nullptr, s_cap = nullptr;  // copy streams (H2D / D2H engines), capture
     cudaStream_t s_k[kKStreams] = {};                                // band kernels (overlapping)
     cudaEvent_t ev_start = nullptr, ev_done = nullptr, ev_in[kMaxBands] = {}, ev_k[kMaxBands] = {};
+    cudaEvent_t ev_out[kMaxBands] = {};  // band k's D2H done (the float64 pipeline's output conversion waits on it)
     GraphEntry graphs[kGraphs];
     unsigned long long tick = 0;
     void drop_graphs()
@@ -430,6 +437,41 @@ int enqueue_bands(HostCache &c, const uint8_t *h_in, int H, int W, uint8_t *h_ou
     return DFG_OK;
 }
 
+// Device staging, streams and events of the host paths (per thread; grows).
+int ensure_host_cache(HostCache &c, size_t px)
+{
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (c.dev != dev || c.px_cap < px) {
+        c.release();
+        cudaError_t e = cudaMalloc(&c.d_in, 3 * px);
+        if (e == cudaSuccess) e = cudaMalloc(&c.d_out, 3 * px);
+        if (e == cudaSuccess) e = cudaMalloc(&c.ws, dfg_workspace_bytes((int64_t)px));
+        if (e == cudaSuccess) e = cudaMemset(c.ws, 0, dfg_workspace_bytes((int64_t)px));
+        if (e == cudaSuccess && c.dev != dev) {
+            e = cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s_cap, cudaStreamNonBlocking);
+            for (int k = 0; k < kKStreams && e == cudaSuccess; k++)
+                e = cudaStreamCreateWithFlags(&c.s_k[k], cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_done, cudaEventDisableTiming);
+            for (int k = 0; k < kMaxBands && e == cudaSuccess; k++) {
+                e = cudaEventCreateWithFlags(&c.ev_in[k], cudaEventDisableTiming);
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_k[k], cudaEventDisableTiming);
+                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_out[k], cudaEventDisableTiming);
+            }
+        }
+        if (e != cudaSuccess) {
+            c.release();
+            return cuda_fail(e, "device staging allocation");
+        }
+        c.px_cap = px;
+        c.dev = dev;
+    }
+    return DFG_OK;
+}
+
 bool is_pinned(const void *p)
 {
     cudaPointerAttributes a;
@@ -451,37 +493,11 @@ int dfg_filter_host(const uint8_t *h_in, int32_t H, int32_t W, uint8_t *h_out, c
     if (rc) return rc;
     if (H < 1 || W < 1) return fail(DFG_E_ARG, "image must contain at least one pixel");
     if (!h_in || !h_out) return fail(DFG_E_ARG, "null host pointer");
-    int dev = 0;
-    cudaGetDevice(&dev);
     HostCache &c = g_host;
     const size_t px = (size_t)H * W;
     cudaStream_t st = (cudaStream_t)stream;
-    if (c.dev != dev || c.px_cap < px) {
-        c.release();
-        cudaError_t e = cudaMalloc(&c.d_in, 3 * px);
-        if (e == cudaSuccess) e = cudaMalloc(&c.d_out, 3 * px);
-        if (e == cudaSuccess) e = cudaMalloc(&c.ws, dfg_workspace_bytes((int64_t)px));
-        if (e == cudaSuccess) e = cudaMemset(c.ws, 0, dfg_workspace_bytes((int64_t)px));
-        if (e == cudaSuccess && c.dev != dev) {
-            e = cudaStreamCreateWithFlags(&c.s_in, cudaStreamNonBlocking);
-            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s_out, cudaStreamNonBlocking);
-            if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c.s_cap, cudaStreamNonBlocking);
-            for (int k = 0; k < kKStreams && e == cudaSuccess; k++)
-                e = cudaStreamCreateWithFlags(&c.s_k[k], cudaStreamNonBlocking);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_start, cudaEventDisableTiming);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_done, cudaEventDisableTiming);
-            for (int k = 0; k < kMaxBands && e == cudaSuccess; k++) {
-                e = cudaEventCreateWithFlags(&c.ev_in[k], cudaEventDisableTiming);
-                if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.ev_k[k], cudaEventDisableTiming);
-            }
-        }
-        if (e != cudaSuccess) {
-            c.release();
-            return cuda_fail(e, "device staging allocation");
-        }
-        c.px_cap = px;
-        c.dev = dev;
-    }
+    rc = ensure_host_cache(c, px);
+    if (rc) return rc;
     const bool pinned = is_pinned(h_in) && is_pinned(h_out);
     const int h = (prm->family == DFG_IDENTITY) ? 0 : prm->window / 2;
     const dfg::Options &opt = dfg::options();
@@ -703,6 +719,122 @@ struct F64Staging {
 };
 thread_local F64Staging g_f64;
 
+// float64 <-> uint8 conversions of the drop-in path: dfg_hostconv.cu
+// Large frames: the conversions run band by band on `threads` host threads
+// around the device pipeline, so the float64 -> uint8 pass of band k + 1
+// overlaps band k's H2D / kernel / D2H, and the uint8 -> float64 pass of
+// band k starts as soon as its D2H has landed (the sequential form -- convert
+// everything, run the pipeline, convert everything back -- costs the sum of
+// the three).  Bands, halo rows and stream roles are those of enqueue_bands.
+// Nothing is written to h_out unless every input value passed the check.
+int f64_pipeline(HostCache &c, F64Staging &g, const double *h_in, int H, int W, double *h_out, const dfg_params *prm,
+                 int threads, cudaStream_t st, int nb)
+{
+    const int h = prm->window / 2;
+    const long long pitch = 3LL * W;
+    const size_t px = (size_t)H * W;
+    auto row0 = [&](int k) { return k >= nb ? H : (int)((long long)k * H / nb); };
+    const int nks = nb < kKStreams ? nb : kKStreams;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaError_t e = cudaEventRecord(c.ev_start, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_in, c.ev_start, 0);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(c.s_out, c.ev_start, 0);
+    for (int k = 0; k < nks && e == cudaSuccess; k++) e = cudaStreamWaitEvent(c.s_k[k], c.ev_start, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "fork");
+
+    const int T = threads < 1 ? 1 : threads;
+    std::atomic<int> in_done[kMaxBands], state[kMaxBands];  // state: 0 pending, 1 enqueued, -1 abandoned
+    for (int k = 0; k < kMaxBands; k++) {
+        in_done[k].store(0);
+        state[k].store(0);
+    }
+    std::atomic<unsigned> bad{0};
+    int rc_enq = DFG_OK;          // thread 0 only
+    cudaError_t e_enq = cudaSuccess;
+    const char *where = "";
+    const int w3_rpc = dfg::options().host_w3_rpc;
+
+    auto enqueue_band = [&](int k) {  // thread 0: H2D, kernel, D2H of band k
+        const int r0 = row0(k), r1 = row0(k + 1);
+        const int c0 = k == 0 ? 0 : r0 + h, c1 = k + 1 == nb ? H : r1 + h;
+        cudaStream_t sk = c.s_k[k % nks];
+        if (c1 > c0)
+            e_enq = cudaMemcpyAsync(c.d_in + c0 * pitch, g.in + c0 * pitch, (size_t)(c1 - c0) * pitch,
+                                    cudaMemcpyHostToDevice, c.s_in);
+        if (e_enq == cudaSuccess) e_enq = cudaEventRecord(c.ev_in[k], c.s_in);
+        if (e_enq == cudaSuccess) e_enq = cudaStreamWaitEvent(sk, c.ev_in[k], 0);
+        if (e_enq != cudaSuccess) { where = "H2D"; return; }
+        rc_enq = run(c.d_in, H, W, 0, H, pitch, 0, c.d_out + r0 * pitch, r0, r1 - r0, pitch, 0, 1, prm, c.ws,
+                     dfg_workspace_bytes((int64_t)px), sk, nullptr, w3_rpc);
+        if (rc_enq) return;
+        e_enq = cudaEventRecord(c.ev_k[k], sk);
+        if (e_enq == cudaSuccess) e_enq = cudaStreamWaitEvent(c.s_out, c.ev_k[k], 0);
+        if (e_enq == cudaSuccess)
+            e_enq = cudaMemcpyAsync(g.out + r0 * pitch, c.d_out + r0 * pitch, (size_t)(r1 - r0) * pitch,
+                                    cudaMemcpyDeviceToHost, c.s_out);
+        if (e_enq == cudaSuccess) e_enq = cudaEventRecord(c.ev_out[k], c.s_out);
+        if (e_enq != cudaSuccess) where = "D2H";
+    };
+    auto slice = [&](size_t lo, size_t hi, int t, size_t &a, size_t &b) {
+        const size_t n = hi - lo, step = (n + T - 1) / T;
+        a = lo + (size_t)t * step;
+        b = a + step;
+        if (a > hi) a = hi;
+        if (b > hi) b = hi;
+    };
+    auto worker = [&](int t) {
+        if (t != 0) cudaSetDevice(dev);
+        // input bands: convert, then thread 0 enqueues the band's device work
+        for (int k = 0; k < nb; k++) {
+            const int r0 = row0(k), r1 = row0(k + 1);
+            const int c0 = k == 0 ? 0 : r0 + h, c1 = k + 1 == nb ? H : r1 + h;
+            size_t a, b;
+            slice((size_t)c0 * pitch, (size_t)c1 * pitch, t, a, b);
+            if (dfg::f64_to_u8(h_in, g.in, a, b)) bad.store(1u, std::memory_order_relaxed);
+            in_done[k].fetch_add(1, std::memory_order_acq_rel);
+            if (t == 0) {
+                while (in_done[k].load(std::memory_order_acquire) < T) std::this_thread::yield();
+                const bool ok = !bad.load() && rc_enq == DFG_OK && e_enq == cudaSuccess;
+                if (ok) enqueue_band(k);
+                state[k].store(ok && rc_enq == DFG_OK && e_enq == cudaSuccess ? 1 : -1, std::memory_order_release);
+            }
+        }
+        // output bands: wait for the band's D2H, convert back.  (The last
+        // input band is checked before any output is written: band nb - 1's
+        // state is set only after every input value has been seen.)
+        while (state[nb - 1].load(std::memory_order_acquire) == 0) std::this_thread::yield();
+        if (state[nb - 1].load() < 0) return;
+        for (int k = 0; k < nb; k++) {
+            if (cudaEventSynchronize(c.ev_out[k]) != cudaSuccess) {
+                bad.store(2u);
+                return;
+            }
+            size_t a, b;
+            slice((size_t)row0(k) * pitch, (size_t)row0(k + 1) * pitch, t, a, b);
+            dfg::u8_to_f64(g.out, h_out, a, b);
+        }
+    };
+    {
+        std::vector<std::thread> pool;
+        pool.reserve(T - 1);
+        for (int t = 1; t < T; t++) pool.emplace_back(worker, t);
+        worker(0);
+        for (std::thread &th : pool) th.join();
+    }
+    // join: later work on `st` sees the result; drain whatever was enqueued
+    e = cudaEventRecord(c.ev_done, c.s_out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, c.ev_done, 0);
+    for (int k = 0; k < nks && e == cudaSuccess; k++) e = cudaStreamSynchronize(c.s_k[k]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.s_in);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c.s_out);
+    if (bad.load() == 1u) return fail(DFG_E_ARG, "pixel values must be integers in 0..255 on the GPU path");
+    if (rc_enq) return rc_enq;
+    if (e_enq != cudaSuccess) return cuda_fail(e_enq, where);
+    if (e != cudaSuccess || bad.load() == 2u) return cuda_fail(e != cudaSuccess ? e : cudaGetLastError(), "float64 pipeline");
+    return DFG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -731,28 +863,38 @@ int dfg_filter_host_f64(const double *h_in, int32_t H, int32_t W, double *h_out,
         }
         g.cap = n;
     }
+#if defined(__linux__)
+    if (n * sizeof(double) >= (64u << 20)) {
+        // a freshly allocated result array is first touched here: ask for huge
+        // pages (2 MiB faults instead of 4 KiB ones; a hint, ignored if disabled)
+        const uintptr_t a = ((uintptr_t)h_out + 4095) & ~(uintptr_t)4095;
+        const uintptr_t b = ((uintptr_t)h_out + n * sizeof(double)) & ~(uintptr_t)4095;
+        if (b > a) madvise((void *)a, b - a, MADV_HUGEPAGE);
+    }
+#endif
+    // large frames: conversions pipelined around the device work, band by band
+    const size_t px = (size_t)H * W;
+    int nb = (int)(px / (1u << 20));
+    if (nb > kMaxBands) nb = kMaxBands;
+    if (nb > H / 64) nb = H / 64;
+    const int h = prm->window / 2;
+    if (prm->border == DFG_REFLECT && H <= 4 * h) nb = 1;
+    if (dfg::options().host_bands > 0) nb = dfg::options().host_bands > kMaxBands ? kMaxBands : dfg::options().host_bands;
+    if (prm->family != DFG_IDENTITY && nb >= 2 && nb <= H / (2 * h + 1)) {
+        rc = ensure_host_cache(g_host, px);
+        if (rc) return rc;
+        return f64_pipeline(g_host, g, h_in, H, W, h_out, prm, threads, (cudaStream_t)stream, nb);
+    }
     // float64 -> uint8 with the GPU path's one input restriction: integral
-    // values in 0..255 (NaN and infinities fail the range test)
+    // values in 0..255
     std::atomic<unsigned> bad{0};
-    uint8_t *st = g.in;
     parallel_ranges(n, threads, [&](size_t lo, size_t hi) {
-        unsigned b = 0;
-        for (size_t i = lo; i < hi; i++) {
-            const double v = h_in[i];
-            const double c = (v >= 0.0 && v <= 255.0) ? v : -1.0;
-            const int iv = (int)c;
-            b |= (unsigned)((double)iv != c) | (unsigned)(iv < 0);
-            st[i] = (uint8_t)iv;
-        }
-        if (b) bad.store(1u, std::memory_order_relaxed);
+        if (dfg::f64_to_u8(h_in, g.in, lo, hi)) bad.store(1u, std::memory_order_relaxed);
     });
     if (bad.load()) return fail(DFG_E_ARG, "pixel values must be integers in 0..255 on the GPU path");
     rc = dfg_filter_host(g.in, H, W, g.out, prm, stream);
     if (rc) return rc;
-    const uint8_t *so = g.out;
-    parallel_ranges(n, threads, [&](size_t lo, size_t hi) {
-        for (size_t i = lo; i < hi; i++) h_out[i] = (double)so[i];
-    });
+    parallel_ranges(n, threads, [&](size_t lo, size_t hi) { dfg::u8_to_f64(g.out, h_out, lo, hi); });
     return DFG_OK;
 }
 

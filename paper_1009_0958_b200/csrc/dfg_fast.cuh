@@ -1652,6 +1652,8 @@ struct Shape {
     // per pair, keeps two CTAs with pixel-pair items: 1.35 vs 1.89 ms);
     // 3x3 BVDF/DDF/VMF: 2 CTAs of 16 warps at 64 registers
     static constexpr bool WIDE = S >= 5 && MINB0 >= 2 && ST == ST_MINIMAX;
+    // (a 12-warp CTA with pixel-pair items measured 40-50 % slower for the
+    // minimax shapes: bvdf 3.08 vs 2.21 ms, ddf 5.27 vs 3.56)
     static constexpr int TR = (S == 3 && !FamT<FAM>::CEN) ? 16 : (WIDE ? 2 * TR0 : TR0);
     static constexpr int MINB = (S == 3 && !FamT<FAM>::CEN) ? 2 : (WIDE ? MINB0 / 2 : MINB0);
 };

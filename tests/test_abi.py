@@ -149,3 +149,32 @@ def test_frame_stream_python_validation():
         filter_host_frames([a], s, out=[a, a])  # one output per frame
     with pytest.raises(ValueError):
         filter_host_frames([np.zeros((4, 5), np.uint8)], s)
+
+
+def test_host_conversions_dispatched_equal_scalar():
+    """float64 <-> uint8 of the drop-in boundary (csrc/dfg_hostconv.cu): the
+    AVX2 form equals the scalar one on every length / alignment, flags every
+    value that is not an integer in 0..255 (NaN, infinities, huge, negative,
+    fractional) and accepts -0.0."""
+    L = _lib.lib()
+    rng = np.random.default_rng(0)
+
+    def run(src):
+        n = src.size
+        fast, ref, back = np.zeros(n, np.uint8), np.zeros(n, np.uint8), np.zeros(n)
+        rc = L.dfg_hostconv_selftest(src.ctypes.data, n, fast.ctypes.data, ref.ctypes.data, back.ctypes.data)
+        return rc, fast, ref, back
+
+    for n in (1, 7, 16, 33, 1000, 100003):
+        for off in (0, 1, 3):
+            src = rng.integers(0, 256, n + off).astype(np.float64)[off:]
+            rc, fast, ref, back = run(src)
+            assert rc == 0 and (fast == ref).all() and (back == src).all(), (n, off, rc)
+            for bad in (0.5, 256.0, -1.0, np.nan, np.inf, -np.inf, 255.0000001, 1e300, -0.25, 2.0 ** 31, 2.0 ** 32 + 5):
+                for pos in (0, n // 2, n - 1):
+                    s2 = src.copy()
+                    s2[pos] = bad
+                    assert run(s2)[0] == 3, (n, off, bad, pos)
+            s2 = src.copy()
+            s2[0] = -0.0
+            assert run(s2)[0] == 0

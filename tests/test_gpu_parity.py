@@ -328,6 +328,42 @@ def test_apply_filter_float64_boundary(cuda):
         apply_filter(RasterImage(base + 0.25), parse_filter_spec("ddf:exact"))
 
 
+@pytest.mark.parametrize("spec,border", [("ddf:exact", "replicate"), ("acwddf:exact:window=5", "reflect"),
+                                         ("ddf:exact:window=7", "replicate"), ("bvdf:minimax:window=9", "reflect")])
+def test_float64_pipeline_bands(cuda, spec, border):
+    """Large frames pipeline the float64 <-> uint8 conversions band by band
+    around the device work (dfg_filter_host_f64 -> f64_pipeline): same
+    pixels as the device path for 2 .. 16 bands (forced on a small frame
+    through DFG_OPT_HOST_BANDS) and at the natural size; a bad value in the
+    LAST band raises and leaves the caller's output untouched."""
+    torch = cuda
+    s = parse_filter_spec(spec)
+    pol = _policy(border)
+    H, W = (300, 211) if "window=9" not in spec else (140, 97)
+    img = synth.noisy_image(H, W, 21, ("uncorrelated", 0.15))
+    want = filter_device(torch.from_numpy(img).cuda(), s, pol).cpu().numpy()
+    ri = RasterImage(img.astype(np.float64))
+    for nb in (2, 3, 7, 16):
+        with _lib.option("host_bands", nb):
+            out = apply_filter(ri, s, pol)
+        assert (out.pixels == want).all(), (spec, nb)
+    a = img.astype(np.float64)
+    a[H - 2, 5, 0] = 17.5
+    with _lib.option("host_bands", 5), pytest.raises(ValueError):
+        apply_filter(_raw_image(a), s, pol)
+    with _lib.option("host_bands", 5):  # and the path is usable again afterwards
+        assert (apply_filter(ri, s, pol).pixels == want).all()
+
+
+def test_float64_pipeline_natural_size(cuda):
+    torch = cuda
+    s = parse_filter_spec("ddf:exact")
+    img = synth.noisy_image(1500, 2100, 22, ("correlated", 0.2))  # 3 bands
+    want = filter_device(torch.from_numpy(img).cuda(), s).cpu().numpy()
+    out = apply_filter(RasterImage(img.astype(np.float64)), s)
+    assert (out.pixels == want).all()
+
+
 def _raw_image(a):
     """A duck-typed image carrying pixels RasterImage itself would reject
     (NaN / inf), to reach the C ABI's own validation."""
