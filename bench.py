@@ -536,8 +536,9 @@ def e2e_single(wl, spec, F, torch, args, full=True):
                            "ms_per_step": round(s_af * 1e3, 3), "h2d_bytes_per_step": fb, "d2h_bytes_per_step": fb,
                            "host_bytes_per_step": 2 * 8 * px_frame * 3,
                            "path": "apply_filter(RasterImage float64) -> RasterImage float64 (C ABI "
-                                   "dfg_filter_host_f64: integrality/range check + conversion on all host cores "
-                                   "into pinned staging, then the dfg_filter_host pipeline; output array "
+                                   "dfg_filter_host_f64: integrality/range check + float64<->uint8 conversion "
+                                   "on all host cores (AVX2) into pinned staging, pipelined band by band around "
+                                   "the H2D / kernel / D2H pipeline for frames of >= 2 Mpixel; output array "
                                    "allocated per call, as the reference does); median of 3 calls"}
     if wl["kind"] == "image" and not big:
         ring = 8
