@@ -1,5 +1,6 @@
 """Attribute a kernel's dynamic instructions and stall samples to the
-barrier-delimited regions of its SASS (ncu source page CSV, scripts/gpu_prof.sh).
+barrier-delimited regions of its SASS (barrier waits to the region the
+barrier ends -- see the note at stall_barrier below) (ncu source page CSV, scripts/gpu_prof.sh).
 usage: python scripts/sass_phases.py src_c5a.csv.gz [units]"""
 import collections
 import csv
@@ -33,7 +34,17 @@ for r in rows[2:]:
     d["s"] += s
     d["ops"][op] += n
     for c in stall_cols:
-        d["st"][c[6:]] += int(r[ix[c]] or 0)
+        v = int(r[ix[c]] or 0)
+        # BAR.SYNC.DEFER_BLOCKING lets a warp run on past the barrier until its
+        # first blocking (memory) instruction, and that is where a warp waiting
+        # for the barrier is sampled: barrier-stall samples belong to the
+        # region the barrier ENDS, i.e. the previous one
+        if c == "stall_barrier" and seg > 0 and not op.startswith("BAR."):
+            segs[seg - 1]["st"]["barrier"] += v
+            segs[seg - 1]["s"] += v
+            d["s"] -= v
+            continue
+        d["st"][c[6:]] += v
     if op.startswith("BAR.SYNC") or op.startswith("BAR.RED") or op.startswith("BAR.ARV"):
         seg += 1
 N = sum(d["n"] for d in segs.values())
