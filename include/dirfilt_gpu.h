@@ -77,7 +77,7 @@ extern "C" {
 #define DFG_OK 0
 #define DFG_E_ARG (-1)     /* invalid argument (maps to the reference's ValueError) */
 #define DFG_E_CUDA (-2)    /* CUDA runtime error */
-#define DFG_E_UNSUP (-3)   /* valid spec outside this build (e.g. window > 7) */
+#define DFG_E_UNSUP (-3)   /* valid spec outside this build (window side > 31) */
 #define DFG_E_WS (-4)      /* workspace too small */
 
 /* Mirrors FilterSpec (filters.py:126-151) + AcwddfParams (filters.py:97-123)
@@ -85,7 +85,7 @@ extern "C" {
 typedef struct dfg_params {
     int32_t family;
     int32_t strategy;
-    int32_t window;      /* odd side s; this build: 3, 5, 7 */
+    int32_t window;      /* odd side s >= 3; this build: up to 31 */
     int32_t border;
     double p;            /* Minkowski order: spec.p, or acwddf.p for ACWDDF (filters.py:398) */
     double asin_c[5];    /* ASIN polynomial a0..a4, zero-padded (minimax only) */
