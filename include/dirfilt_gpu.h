@@ -179,7 +179,6 @@ DFG_API int dfg_filter_host_frames(const uint8_t *const *h_in, uint8_t *const *h
 #define DFG_OPT_W3_SMALL_WPS 9  /* 3x3 row sweep: warps per SM for single-wave frames (default 12) */
 #define DFG_OPT_CR_MARGIN 10    /* relative margin below which the correctly rounded arccos pass runs */
 #define DFG_OPT_PERSIST 12      /* CTA kernels as one wave of persistent CTAs (default 1; 0: one tile per CTA) */
-#define DFG_OPT_SWEEP 13        /* 5x5 / 7x7 BVDF, DDF, VMF: 1 = the row-sweeping pixel-owner kernel */
 #define DFG_OPT_TMA 11          /* CTA-kernel tiles by bulk tensor copies: bit 0 input, bit 1 output (default 3) */
 DFG_API int dfg_set_option(int32_t key, double value);
 DFG_API double dfg_get_option(int32_t key);

@@ -125,7 +125,7 @@ def lib() -> ctypes.CDLL:
 
 # schedule / diagnostic options (DFG_OPT_* in include/dirfilt_gpu.h)
 OPTIONS = {"s3_schedule": 1, "no_fixup": 2, "host_bands": 3, "host_graph": 4, "host_w3_rpc": 5,
-           "frame_slots": 6, "w3_wps": 7, "w3_rpc": 8, "w3_small_wps": 9, "cr_margin": 10, "tma": 11, "persist": 12, "sweep": 13}
+           "frame_slots": 6, "w3_wps": 7, "w3_rpc": 8, "w3_small_wps": 9, "cr_margin": 10, "tma": 11, "persist": 12}
 
 
 def set_option(name: str, value) -> float:

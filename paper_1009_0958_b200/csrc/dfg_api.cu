@@ -331,7 +331,6 @@ int dfg_set_option(int32_t key, double value)
     case DFG_OPT_CR_MARGIN: o.cr_margin = value; break;
     case DFG_OPT_TMA: o.tma = v; break;
     case DFG_OPT_PERSIST: o.persist = v; break;
-    case DFG_OPT_SWEEP: o.sweep = v; break;
     default: return fail(DFG_E_ARG, "unknown option key");
     }
     g_host.drop_graphs();  // captured pipelines bake the old settings in
@@ -354,7 +353,6 @@ double dfg_get_option(int32_t key)
     case DFG_OPT_CR_MARGIN: return o.cr_margin;
     case DFG_OPT_TMA: return o.tma;
     case DFG_OPT_PERSIST: return o.persist;
-    case DFG_OPT_SWEEP: return o.sweep;
     default: return NAN;
     }
 }

@@ -1632,8 +1632,6 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
 // state per output is n (BVDF/VMF), 2n (DDF, CWVMF) or 4n (ACWDDF, CWDDF) floats.
 template <int FAM, int ST, int PC>
 cudaError_t launch_w3(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp);  // dfg_w3.cuh
-template <int S, int FAM, int ST, int PC>
-cudaError_t launch_sweep(cudaStream_t st, const uint8_t *in, uint8_t *out, const KParams &kp);  // dfg_sweep.cuh
 
 template <int S, int FAM, int ST>
 struct Shape {
@@ -1675,11 +1673,6 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
                         (force ? force == 1 : (kp.w3_rpc > 0 || strip_rows >= 8192));
         if (w3) return launch_w3<FAM, ST, PC>(st, in, out, kp);
     }
-    if constexpr (S >= 5 && !FamT<FAM>::CEN) {
-        // 5x5 / 7x7 BVDF, DDF, VMF: the row-sweeping pixel-owner kernel
-        // (dfg_sweep.cuh) where the option selects it
-        if (options().sweep) return launch_sweep<S, FAM, ST, PC>(st, in, out, kp);
-    }
     using SH = Shape<S, FAM, ST>;
     using C = Cfg<S, FAM, SH::OPT, SH::TR>;
     auto kern = dfg_fast_kernel<S, FAM, ST, PC, SH::OPT, SH::TR, SH::MINB>;
@@ -1710,8 +1703,6 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
 }
 
 }  // namespace dfg
-
-#include "dfg_sweep.cuh"
 
 // Family launcher bodies: dispatch strategy x Minkowski order, instantiating
 // only the combinations a family can use.

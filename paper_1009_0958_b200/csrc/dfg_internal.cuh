@@ -88,7 +88,6 @@ struct Options {
     int w3_small_wps = 12;  // DFG_OPT_W3_SMALL_WPS: warps per SM for single-wave 3x3 frames
     double cr_margin = 1e-12;  // DFG_OPT_CR_MARGIN: relative margin that triggers the CR-acos pass
     int persist = 1;        // DFG_OPT_PERSIST: CTA kernels as one wave of persistent CTAs (0: one tile per CTA)
-    int sweep = 0;          // DFG_OPT_SWEEP: 5x5 / 7x7 BVDF / DDF / VMF on the row-sweeping pixel-owner kernel
     int tma = 3;            // DFG_OPT_TMA: bulk tensor copies of the CTA kernels' tiles: 1 input, 2 output, 3 both
 };
 Options &options();
