@@ -394,3 +394,40 @@ def test_tile_bulk_copies_on_and_off(cuda, spec, tma):
     for i in range(3):
         assert (gotb[i] == oracle.filter_image(frames[i], s)).all(), (spec, tma, i)
     assert (gots == want[40:136]).all(), (spec, tma)
+
+
+def test_strip_job_cuda_kernel_single_rank_nccl(cuda):
+    """parallel.filter_strips -- the step bench.py times at N > 1 -- with its
+    default CUDA strip filter (dfg_filter_rows per row chunk) under a real
+    NCCL group of one rank, gather on and off: equals the whole-frame call.
+    (Several ranks need several GPUs; the collective logic itself is covered
+    at world sizes 2..8 with gloo in tests/test_parallel.py, and a 4-rank
+    partition is emulated here rank by rank through the same StripJob row
+    bounds with hand-cut halos.)"""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1009_0958_b200.parallel import filter_strips, strip_rows
+
+    torch = cuda
+    spec = parse_filter_spec("ddf:exact:window=7")
+    img = synth.noisy_image(700, 301, 31, ("correlated", 0.2))
+    x = torch.from_numpy(img).cuda()
+    want = filter_device(x, spec)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        for gather in (True, False):
+            got = filter_strips(x, 0, 700, 700, spec, REPLICATE, gather=gather, chunks=4)
+            torch.cuda.synchronize()
+            assert (got == want).all(), gather
+    finally:
+        dist.destroy_process_group()
+    # a 4-rank partition, one "rank" at a time on this GPU
+    for rank in range(4):
+        r0, r1, i0, i1 = strip_rows(700, 4, rank, 7)
+        out = filter_rows_device(x[i0:i1].contiguous(), 700, i0, r0, r1 - r0, spec)
+        assert (out == want[r0:r1]).all(), rank
