@@ -26,8 +26,9 @@ LIB = PKG / "libdfg.so"
 INCLUDE = PKG.parent / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = [*os.environ.get("DFG_DEFS", "").split(), "-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-          f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
+# (DFG_DEFS: extra -D flags for measurement builds, scripts/dev_unit.py; empty in product builds)
+COMMON = [*os.environ.get("DFG_DEFS", "").split(), "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
+          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", f"-I{INCLUDE}", "--expt-relaxed-constexpr"]
 PER_FILE: dict = {}
 
 
