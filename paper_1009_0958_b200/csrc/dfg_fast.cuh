@@ -1741,12 +1741,28 @@ cudaError_t launch_fast(cudaStream_t st, const uint8_t *in, uint8_t *out, const 
         DFG_P_SWITCH(S, dfg::FAM_BVDF, dfg::ST_CHROMA)                              \
     }
 
-#define DFG_DEFINE_LAUNCH_PAIRED(S, FAM, FAMNAME)                                   \
+// DDF / ACWDDF / CWDDF: 3 strategies x 3 Minkowski orders.  One translation
+// unit per Minkowski order (build time: the 7x7 kernels take ~30 s each):
+// ..._PC defines that order's launcher, ..._DISPATCH (in the p = 2 unit) the
+// family launcher over the three.
+#define DFG_DEFINE_LAUNCH_PAIRED_PC(S, FAM, FAMNAME, PCNAME, PC)                    \
+    cudaError_t dfg_launch_s##S##_##FAMNAME##_##PCNAME(int strategy, cudaStream_t st, \
+                                                       const uint8_t *in, uint8_t *out, \
+                                                       const dfg::KParams &kp)      \
+    {                                                                               \
+        if (strategy == dfg::ST_EXACT) return dfg::launch_fast<S, FAM, dfg::ST_EXACT, PC>(st, in, out, kp); \
+        if (strategy == dfg::ST_MINIMAX) return dfg::launch_fast<S, FAM, dfg::ST_MINIMAX, PC>(st, in, out, kp); \
+        return dfg::launch_fast<S, FAM, dfg::ST_CHROMA, PC>(st, in, out, kp);       \
+    }
+
+#define DFG_DEFINE_LAUNCH_PAIRED_DISPATCH(S, FAMNAME)                               \
+    cudaError_t dfg_launch_s##S##_##FAMNAME##_p1(int, cudaStream_t, const uint8_t *, uint8_t *, const dfg::KParams &); \
+    cudaError_t dfg_launch_s##S##_##FAMNAME##_pgen(int, cudaStream_t, const uint8_t *, uint8_t *, const dfg::KParams &); \
     cudaError_t dfg_launch_s##S##_##FAMNAME(int strategy, int pcode, cudaStream_t st, \
                                             const uint8_t *in, uint8_t *out,        \
                                             const dfg::KParams &kp)                 \
     {                                                                               \
-        if (strategy == dfg::ST_EXACT) { DFG_P_SWITCH(S, FAM, dfg::ST_EXACT) }      \
-        if (strategy == dfg::ST_MINIMAX) { DFG_P_SWITCH(S, FAM, dfg::ST_MINIMAX) }  \
-        DFG_P_SWITCH(S, FAM, dfg::ST_CHROMA)                                        \
+        if (pcode == dfg::PC_2) return dfg_launch_s##S##_##FAMNAME##_p2(strategy, st, in, out, kp); \
+        if (pcode == dfg::PC_1) return dfg_launch_s##S##_##FAMNAME##_p1(strategy, st, in, out, kp); \
+        return dfg_launch_s##S##_##FAMNAME##_pgen(strategy, st, in, out, kp);       \
     }

@@ -1,0 +1,3 @@
+// Instantiation unit: window 5x5, ACWDDF (_engine.py:451-487), general Minkowski order p.
+#include "dfg_fast.cuh"
+DFG_DEFINE_LAUNCH_PAIRED_PC(5, dfg::FAM_ACWDDF, acwddf, pgen, dfg::PC_GEN)

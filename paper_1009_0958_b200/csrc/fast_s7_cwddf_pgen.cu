@@ -1,0 +1,3 @@
+// Instantiation unit: window 7x7, CWDDF (centre-weighted DDF applied to every window, filters.py:296-328), general Minkowski order p.
+#include "dfg_fast.cuh"
+DFG_DEFINE_LAUNCH_PAIRED_PC(7, dfg::FAM_CWDDF, cwddf, pgen, dfg::PC_GEN)

@@ -1,0 +1,3 @@
+// Instantiation unit: window 7x7, DDF (_engine.py:435-448), general Minkowski order p.
+#include "dfg_fast.cuh"
+DFG_DEFINE_LAUNCH_PAIRED_PC(7, dfg::FAM_DDF, ddf, pgen, dfg::PC_GEN)
