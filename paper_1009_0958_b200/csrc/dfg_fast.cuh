@@ -1068,11 +1068,20 @@ __device__ __forceinline__ void seg_stages(const float4 *rec, typename Cfg<S, FA
                     T[t] = sD[(NDV - 1 - t) * RN + qi - du * RW + dv];
                 }
             }
-            DT Sg[S];
-            seg_sums<S>(T, Sg);
-            DT *dst = sM;
+            // seg_sums' operations and order, each sum stored as it completes
+            // (prefix sums R of the right part, then the suffix sums L of the
+            // left part descending: Sg[v] = L[S-1-v] + R[S-1-v])
+            DT R[S];
+            R[0] = T[S - 1];
 #pragma unroll
-            for (int v = 0; v < S; v++) dst[v * RN + qi] = Sg[v];
+            for (int k = 1; k < S; k++) R[k] = dt_add(R[k - 1], T[S - 1 + k]);
+            sM[qi] = R[S - 1];  // v = 0
+            DT L = T[S - 2];
+#pragma unroll
+            for (int k = S - 2; k >= 0; k--) {
+                if (k < S - 2) L = dt_add(T[k], L);
+                sM[(S - 1 - k) * RN + qi] = dt_add(L, R[k]);
+            }
         }
         if constexpr (CEN) {  // centre-column stash: the pair (i, centre) itself
 #pragma unroll
@@ -1240,6 +1249,14 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         s_tile[par][2] = T.frame;
         s_tile[par][3] = T.inside;
     };
+    if constexpr (C::SEG) {
+        // parity records: every element starts as the neutral gray pair (the pad
+        // halves are never written again)
+        for (int i = threadIdx.x; i < 2 * C::RECN2; i += NT) {
+            sA[i] = make_float4(1.f, 1.f, 1.f, 1.f);
+            sA[2 * C::RECN2 + i] = make_float4(1.f, 1.f, pad_aux, pad_aux);
+        }
+    }
     int t = blockIdx.x;
     if (threadIdx.x == 0) {
         mbar_init(&s_bar[0], 1);
@@ -1282,13 +1299,25 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         static_assert((size_t)C::NPL * RN * sizeof(DT) >= (size_t)RN * sizeof(float4), "staging temp fits");
         const bool from_tma = kp.tma_in && T.inside;
         bool any_zero = false;
-        auto norm = [&](int idx, uint32_t r8, uint32_t g8, uint32_t b8) {
+        auto norm = [&](int idx, int ry, int rx, uint32_t r8, uint32_t g8, uint32_t b8) {
             const bool zero = (r8 | g8 | b8) == 0;
             any_zero |= zero;
             const float gx = zero ? 1.f : (float)r8, gy = zero ? 1.f : (float)g8, gz = zero ? 1.f : (float)b8;
             const float aux = encode_aux<ST, C::NEED_L>(gx, gy, gz, zero);
             sK[idx] = r8 | (g8 << 8) | (b8 << 16);
-            tmp[idx] = make_float4(gx, gy, gz, aux);
+            if constexpr (C::SEG) {
+                // straight into the parity records: the pixel is the first half
+                // of element (rx, rx+1) [parity rx & 1] and the second half of
+                // element (rx-1, rx) [the other parity]; pad halves keep the
+                // neutral pixel written once at kernel start
+                float *a1 = reinterpret_cast<float *>(sA + (rx & 1) * C::RECN2 + ry * C::RWS2 + (rx >> 1) + C::PADE);
+                float *a2 = reinterpret_cast<float *>(sA + ((rx + 1) & 1) * C::RECN2 + ry * C::RWS2 + ((rx + 1) >> 1) - 1 +
+                                                      C::PADE);
+                a1[0] = gx; a1[2] = gy; a1[8 * C::RECN2] = gz; a1[8 * C::RECN2 + 2] = aux;
+                a2[1] = gx; a2[3] = gy; a2[8 * C::RECN2 + 1] = gz; a2[8 * C::RECN2 + 3] = aux;
+            } else {
+                tmp[idx] = make_float4(gx, gy, gz, aux);
+            }
         };
         // the bulk store of two tiles ago (same parity) has read its sOut buffer
         if (tid == 0 && kp.tma_out) tma_store_wait_read1();
@@ -1299,7 +1328,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             for (int idx = tid; idx < RN; idx += NT) {
                 const int ry = idx / RW, rx = idx - ry * RW;
                 const uint8_t *px = raw + ry * C::kRawPitch + 3 * rx;
-                norm(idx, px[0], px[1], px[2]);
+                norm(idx, ry, rx, px[0], px[1], px[2]);
             }
         } else {  // indexed loads, border policy by index resolution
             const uint8_t *fin = in + (long long)frame * kp.in_fstride;
@@ -1315,7 +1344,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                     gxx = resolve_idx(tile_x0 + rx - H, kp.W, kp.border);
                 }
                 const uint8_t *px = fin + (long long)gyy * kp.in_pitch + gxx * 3;
-                norm(idx, px[0], px[1], px[2]);
+                norm(idx, ry, rx, px[0], px[1], px[2]);
             }
         }
         // zero vectors (raw 0 vs gray-mapped 1) only matter to the Minkowski term
@@ -1334,19 +1363,7 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
             }
             s_state = st ^ 1u;  // read again only after the tile's last barrier
         }
-        if constexpr (C::SEG) {
-            // parity layout: element e of parity row (par, ry) = columns c, c+1,
-            // c = 2 (e - PADE) + par; arrays A-even, A-odd, B-even, B-odd
-            for (int idx = tid; idx < 2 * C::RECN2; idx += NT) {
-                const int par = idx >= C::RECN2 ? 1 : 0, k = idx - par * C::RECN2;
-                const int ry = k / C::RWS2, e = k - ry * C::RWS2;
-                const int r0 = 2 * (e - C::PADE) + par, r1 = r0 + 1;
-                const float4 f = (r0 >= 0 && r0 < RW && ry < RH) ? tmp[ry * RW + r0] : neutral;
-                const float4 s = (r1 >= 0 && r1 < RW && ry < RH) ? tmp[ry * RW + r1] : neutral;
-                sA[idx] = make_float4(f.x, s.x, f.y, s.y);
-                sA[2 * C::RECN2 + idx] = make_float4(f.z, s.z, f.w, s.w);
-            }
-        } else {
+        if constexpr (!C::SEG) {
             for (int idx = tid; idx < C::RECN; idx += NT) {
                 const int ry = idx / RWS, c = idx - ry * RWS;
                 const int r0 = c - PADC, r1 = r0 + 1;
@@ -1355,8 +1372,8 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
                 sA[idx] = make_float4(f.x, s.x, f.y, s.y);
                 sB[idx] = make_float4(f.z, s.z, f.w, s.w);
             }
+            __syncthreads();
         }
-        __syncthreads();
 
         // aggregates: BOTH -> packed (angular, Minkowski) pairs; else scalars
         P2 ag[OPT][BOTH ? N : 1];
