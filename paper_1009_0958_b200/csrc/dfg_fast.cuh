@@ -1291,10 +1291,12 @@ dfg_fast_kernel(const uint8_t *__restrict__ in, uint8_t *__restrict__ out, const
         if (tid == 0) s_nflag = 0;
 
         // ---- stage 0: region staging + per-pixel normalisation ------------
-        // Pass 1 normalises every region pixel into a temporary float4
-        // record (in the plane buffer, free at this point); pass 2 assembles
-        // the pair elements (c, c+1) with whole 16-byte stores.  Pad
-        // positions hold a neutral gray pixel.
+        // Every region pixel is normalised once.  5x5 / 7x7: its four values
+        // go straight into the two parity elements that contain it.  3x3: into
+        // a temporary float4 record (in the plane buffer, free at this
+        // point), from which a second pass assembles the pair elements
+        // (c, c+1) with whole 16-byte stores.  Pad positions hold a neutral
+        // gray pixel.
         float4 *tmp = reinterpret_cast<float4 *>(sD);
         static_assert((size_t)C::NPL * RN * sizeof(DT) >= (size_t)RN * sizeof(float4), "staging temp fits");
         const bool from_tma = kp.tma_in && T.inside;
