@@ -23,6 +23,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libdfg.so"
+DEV_MARK = PKG / ".dev_build"
 INCLUDE = PKG.parent / "include"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -47,6 +48,11 @@ def _headers_mtime() -> float:
 def build(verbose: bool = False, force: bool = False, jobs: int | None = None) -> Path:
     sources = sorted(CSRC.glob("*.cu"))
     hdr = _headers_mtime()
+    # scripts/dev_unit.py leaves this marker: the library then holds a partial
+    # (measurement) instantiation of some unit and must not pass for a product
+    # build -- unless the measurement scripts say so
+    if DEV_MARK.exists() and os.environ.get("DFG_ALLOW_DEV_LIB") != "1":
+        force = True
     if not force and LIB.exists() and LIB.stat().st_mtime >= max([hdr] + [s.stat().st_mtime for s in sources]):
         return LIB  # up to date (e.g. the prebuilt library shipped to a GPU box without its objects)
     nvcc = _nvcc()
@@ -82,6 +88,8 @@ def build(verbose: bool = False, force: bool = False, jobs: int | None = None) -
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
         os.replace(tmp, LIB)
+    if force and DEV_MARK.exists():
+        DEV_MARK.unlink()
     return LIB
 
 

@@ -40,3 +40,4 @@ objs = [b.OBJ / (s.stem + ".o") for s in sorted(b.CSRC.glob("*.cu"))]
 r = subprocess.run([nv, *b.ARCH, "-shared", "-o", str(b.LIB), *map(str, objs), "-cudart", "static"],
                    capture_output=True, text=True)
 print("link", r.returncode, r.stderr[-300:])
+b.DEV_MARK.write_text("partial instantiation by scripts/dev_unit.py: run `python -m paper_1009_0958_b200.build -f`\n")
