@@ -431,3 +431,24 @@ def test_strip_job_cuda_kernel_single_rank_nccl(cuda):
         r0, r1, i0, i1 = strip_rows(700, 4, rank, 7)
         out = filter_rows_device(x[i0:i1].contiguous(), 700, i0, r0, r1 - r0, spec)
         assert (out == want[r0:r1]).all(), rank
+
+
+@pytest.mark.parametrize("threads", [1, 3, 64])
+def test_float64_path_thread_counts(cuda, threads):
+    """dfg_filter_host_f64 with explicit host thread counts (the Python shim
+    passes 0 = all cores), banded and unbanded: same pixels."""
+    import ctypes
+
+    torch = cuda
+    spec = parse_filter_spec("acwddf:exact")
+    img = synth.noisy_image(260, 190, 33, ("uncorrelated", 0.1))
+    want = filter_device(torch.from_numpy(img).cuda(), spec).cpu().numpy().astype(np.float64)
+    a = img.astype(np.float64)
+    prm = _lib.params_from_spec(spec, "replicate")
+    for nb in (0, 4):
+        out = np.full(a.shape, -1.0)
+        with _lib.option("host_bands", nb):
+            rc = _lib.lib().dfg_filter_host_f64(a.ctypes.data_as(ctypes.c_void_p), 260, 190,
+                                                out.ctypes.data_as(ctypes.c_void_p), ctypes.byref(prm), threads, None)
+        _lib.check(rc)
+        assert (out == want).all(), (threads, nb)
